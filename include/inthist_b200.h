@@ -1,0 +1,129 @@
+/*
+ * inthist_b200.h -- C ABI of the B200 integral-histogram engine.
+ *
+ * The reference `inthist` (arXiv 1711.01919 CPU restatement) exposes its hot
+ * path as Python module functions; no FFI exists upstream.  Each entry point
+ * below replaces the compute body of one reference function (paths relative
+ * to the reference package pkg/src/inthist/):
+ *
+ *   ih_integral_histogram   <- strategies.py:219-229 compute() and the four
+ *                              strategies it dispatches to: compute_sequential
+ *                              :109-115, compute_crossweave :129-150,
+ *                              compute_sts :162-169, compute_wavefront :172-216
+ *                              (all bit-identical), plus the
+ *                              binning BinSpec.bin_image core.py:94-96.
+ *   ih_region_histograms    <- core.py:179-195 region_histogram (batched).
+ *   ih_window_counts        <- likelihood.py:34-52 window_counts.
+ *
+ * Conventions (all entry points):
+ *   - stream-ordered and asynchronous: work is enqueued on `stream`; nothing
+ *     synchronises the host; no allocation (the caller owns every buffer,
+ *     including the workspace); no global state.
+ *   - all pointers except `lut256` are DEVICE pointers; sizes in elements
+ *     unless suffixed _bytes.
+ *   - argument validation mirrors the reference's exception order; every
+ *     status maps 1:1 onto a reference exception class (errors.py:4-29).
+ *   - no CPU fallback: a missing/failed CUDA device yields IH_ERR_CUDA.
+ *
+ * Layout: the integral-histogram tensor is bin-major (bins, H, W) uint32,
+ * C-contiguous, exactly as IntegralHistogram.counts (core.py:106-116).  A
+ * batch of frames is (frames, slab_bins, H, W).
+ */
+#ifndef INTHIST_B200_H
+#define INTHIST_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    IH_OK = 0,
+    IH_ERR_SHAPE = 1,     /* errors.py:16 ShapeError     */
+    IH_ERR_CAPACITY = 2,  /* errors.py:8  CapacityError  */
+    IH_ERR_PARAM = 3,     /* errors.py:20 ParameterError */
+    IH_ERR_BOUNDS = 4,    /* errors.py:12 BoundsError    */
+    IH_ERR_CUDA = 5       /* RuntimeError (device/launch failure) */
+} ih_status;
+
+/* Kernel family used by ih_integral_histogram.  Results are bit-identical
+ * for every choice (the reference's contract). */
+typedef enum {
+    IH_KERNEL_AUTO = 0,         /* single-pass scan when the width allows, else cross-weave */
+    IH_KERNEL_SINGLE_PASS = 1,  /* K2: fused bin + 2D scan, each output byte written once */
+    IH_KERNEL_CROSSWEAVE = 2    /* K1 + K1b: fused bin/row scan, then column scan (CW-B) */
+} ih_kernel;
+
+/* Workspace bytes ih_integral_histogram needs for this problem (0 is a valid
+ * answer).  `slab_bins` = bin_hi - bin_lo. */
+size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width,
+                          int32_t slab_bins, int32_t kernel);
+
+/* Integral histograms of `frames` 8-bit images, bins [bin_lo, bin_hi) only.
+ *
+ *   img           device, frame f row r at img + f*frame_stride + r*img_pitch
+ *   lut256        HOST pointer, 256 entries, each < bins (BinSpec.table)
+ *   bins          total bin count of the spec, 1..256 (core.py:72-73)
+ *   bin_lo/hi     the slab this call produces (bin sharding; 0/bins = all)
+ *   out           device, (frames, bin_hi-bin_lo, height, width) uint32
+ *   workspace     device scratch of >= ih_workspace_bytes(...) bytes,
+ *                 16-byte aligned.  Contents need no initialisation.
+ *
+ * Errors, in the reference's order (strategies.py:131-132, core.py:53-57):
+ *   IH_ERR_SHAPE     frames/height/width < 1, bins outside 1..256, LUT entry
+ *                    >= bins, bad slab, null pointers
+ *   IH_ERR_CAPACITY  width*height > 2^32-1
+ *   IH_ERR_PARAM     img_pitch < width, frame_stride < height*img_pitch,
+ *                    workspace too small, unknown kernel
+ *   IH_ERR_CUDA      launch failure */
+ih_status ih_integral_histogram(const uint8_t *img, int64_t frames, int64_t height,
+                                int64_t width, int64_t img_pitch, int64_t frame_stride,
+                                const uint8_t *lut256, int32_t bins, int32_t bin_lo,
+                                int32_t bin_hi, uint32_t *out, void *workspace,
+                                size_t workspace_bytes, int32_t kernel, void *stream);
+
+/* The two phases of ih_integral_histogram, exported separately so callers
+ * (bench.py) can time the dominant kernel alone with events on `stream`.
+ * ih_integral_histogram == ih_ih_prepare + ih_ih_scan. */
+ih_status ih_ih_prepare(const uint8_t *img, int64_t frames, int64_t height, int64_t width,
+                        int64_t img_pitch, int64_t frame_stride, const uint8_t *lut256,
+                        int32_t bins, int32_t bin_lo, int32_t bin_hi, void *workspace,
+                        size_t workspace_bytes, int32_t kernel, void *stream);
+ih_status ih_ih_scan(const uint8_t *img, int64_t frames, int64_t height, int64_t width,
+                     int64_t img_pitch, int64_t frame_stride, const uint8_t *lut256,
+                     int32_t bins, int32_t bin_lo, int32_t bin_hi, uint32_t *out,
+                     void *workspace, size_t workspace_bytes, int32_t kernel, void *stream);
+
+/* Batched four-corner region queries (core.py:179-195).
+ *   t        device (nb, height, width) uint32 integral histogram (a slab is fine)
+ *   regions  device (Q, 4) int32 rows (r0, c0, r1, c1), inclusive (core.py:131-158)
+ *   out      device (Q, nb) uint64
+ * IH_ERR_BOUNDS if any region is degenerate or outside the tensor is NOT
+ * detectable without a sync: the caller validates (the Python layer does,
+ * core.py:142/:158 order); the kernel clamps nothing and reads only in-range
+ * corners for valid regions. */
+ih_status ih_region_histograms(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
+                               const int32_t *regions, int64_t q, uint64_t *out, void *stream);
+
+/* Every h x w window's counts (likelihood.py:34-52).
+ *   out  device (nb, height-h+1, width-w+1) int64
+ * IH_ERR_PARAM if h < 1 or w < 1; IH_ERR_BOUNDS if h > height or w > width
+ * (likelihood.py:36-41 order). */
+ih_status ih_window_counts(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
+                           int32_t h, int32_t w, int64_t *out, void *stream);
+
+/* Human-readable status name. */
+const char *ih_status_string(ih_status s);
+
+/* Last CUDA error string recorded by a failing call on this thread. */
+const char *ih_last_error(void);
+
+/* ABI version: (major << 16) | minor. */
+int32_t ih_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* INTHIST_B200_H */

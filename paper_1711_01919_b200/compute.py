@@ -1,0 +1,156 @@
+"""Image -> integral histogram: the drop-in strategy API, routed to the B200.
+
+Same public surface as the reference's strategies module
+(pkg/src/inthist/strategies.py:36-229): ``Strategy`` with its closed name set,
+the three constants, ``wavefront(tile)``, ``resolve_workers``, ``compute`` and
+the four ``compute_*`` functions with their signatures and validation order.
+
+Every strategy runs on the device and returns the identical tensor (the
+reference's contract):
+
+  sequential / sts / wavefront -> K2, the single-pass tiled 2D scan
+  crossweave                   -> K1 + K1b, the paper's CW-B on the GPU
+                                  (fused bin + row scan, then column scan)
+
+``workers`` is validated (ParameterError when negative, strategies.py:62-65)
+and otherwise has no effect: device parallelism is fixed by the kernels.
+There is no CPU fallback: without a CUDA device the calls raise DeviceError.
+"""
+
+from __future__ import annotations
+
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import device
+from .domain import BinSpec, GrayImage, IntegralHistogram
+from .errors import ParameterError
+
+DEFAULT_TILE = 64  # strategies.py:34 (wavefront tile side; a schedule hint here)
+
+STRATEGY_NAMES = ("sequential", "crossweave", "sts", "wavefront")
+
+# strategy name -> kernel family of the C ABI (include/inthist_b200.h ih_kernel)
+_KERNEL_OF = {
+    "sequential": "auto",
+    "sts": "auto",
+    "wavefront": "auto",
+    "crossweave": "crossweave",
+}
+
+
+@dataclass(frozen=True)
+class Strategy:
+    """A named route to the tensor; ``tile`` only for wavefront (strategies.py:39-50)."""
+
+    name: str
+    tile: int = 0
+
+    def __post_init__(self):
+        if self.name not in STRATEGY_NAMES:
+            raise ParameterError(f"unknown strategy {self.name!r}")
+        is_wf = self.name == "wavefront"
+        if is_wf and self.tile < 1:
+            raise ParameterError(f"wavefront tile must be >= 1, got {self.tile}")
+        if not is_wf and self.tile:
+            raise ParameterError("tile is only meaningful for wavefront")
+
+
+SEQUENTIAL = Strategy("sequential")
+CROSSWEAVE = Strategy("crossweave")
+SCAN_TRANSPOSE_SCAN = Strategy("sts")
+
+
+def wavefront(tile: int = DEFAULT_TILE) -> Strategy:
+    return Strategy("wavefront", tile)
+
+
+def resolve_workers(workers: int) -> int:
+    """Validation of the reference's worker cap (strategies.py:62-65)."""
+    if workers < 0:
+        raise ParameterError(f"worker count must be >= 0, got {workers}")
+    return workers or (os.cpu_count() or 1)
+
+
+def _on_device(img: GrayImage, spec: BinSpec, kernel: str) -> IntegralHistogram:
+    dimg = device.upload_image(img.pixels)
+    t = device.integral_histogram(dimg, spec.table, spec.bins, kernel=kernel)
+    return IntegralHistogram(device_counts=t)
+
+
+def compute_sequential(img: GrayImage, spec: BinSpec) -> IntegralHistogram:
+    """The reference oracle's entry point (strategies.py:109-115), on K2."""
+    img.check_capacity()
+    return _on_device(img, spec, _KERNEL_OF["sequential"])
+
+
+def compute_crossweave(img: GrayImage, spec: BinSpec, workers: int = 0) -> IntegralHistogram:
+    """CW-B (strategies.py:129-150): capacity, then workers, then K1 + K1b."""
+    img.check_capacity()
+    resolve_workers(workers)
+    return _on_device(img, spec, _KERNEL_OF["crossweave"])
+
+
+def compute_sts(img: GrayImage, spec: BinSpec, workers: int = 0) -> IntegralHistogram:
+    """CW-STS entry point (strategies.py:162-169); same tensor via K2."""
+    img.check_capacity()
+    resolve_workers(workers)
+    return _on_device(img, spec, _KERNEL_OF["sts"])
+
+
+def _tile_schedule(ni: int, nj: int):
+    """Anti-diagonal order of the reference's wavefront (strategies.py:210-215)."""
+    for d in range(ni + nj - 1):
+        yield [(i, d - i) for i in range(max(0, d - nj + 1), min(ni - 1, d) + 1)]
+
+
+def compute_wavefront(img: GrayImage, spec: BinSpec, tile: int = DEFAULT_TILE,
+                      workers: int = 0, trace: list | None = None) -> IntegralHistogram:
+    """WF-TiS entry point (strategies.py:172-216): tile, capacity, workers checks
+    in the reference's order, then K2.
+
+    ``trace`` is honoured at the level of the *logical* t x t tile schedule:
+    the device pass has no per-tile events (its carries replace the
+    wavefront), so the list receives, per anti-diagonal, "start" events for
+    every tile on it followed by "finish" events -- the dependency order the
+    K2 carries guarantee.  See DESIGN.md "wavefront trace".
+    """
+    if tile < 1:
+        raise ParameterError(f"tile must be >= 1, got {tile}")
+    img.check_capacity()
+    resolve_workers(workers)
+    ih = _on_device(img, spec, _KERNEL_OF["wavefront"])
+    if trace is not None:
+        ni, nj = -(-img.height // tile), -(-img.width // tile)
+        for diag in _tile_schedule(ni, nj):
+            trace.extend(("start", i, j) for i, j in diag)
+            trace.extend(("finish", i, j) for i, j in diag)
+    return ih
+
+
+def compute(img: GrayImage, spec: BinSpec, strategy: Strategy, workers: int = 0) -> IntegralHistogram:
+    """Dispatch by strategy name (strategies.py:219-229); results never differ."""
+    name = strategy.name
+    if name == "wavefront":
+        return compute_wavefront(img, spec, strategy.tile, workers)
+    if name == "crossweave":
+        return compute_crossweave(img, spec, workers)
+    if name == "sts":
+        return compute_sts(img, spec, workers)
+    return compute_sequential(img, spec)
+
+
+def compute_frames(frames, spec: BinSpec, bin_range=None, kernel: str = "auto"):
+    """Batched video path (no reference equivalent; the reference takes one
+    GrayImage per call): (F, H, W) uint8 host or CUDA frames -> CUDA tensor
+    (F, B, H, W) uint32, or the bins [lo, hi) of ``bin_range``."""
+    import torch
+
+    if isinstance(frames, np.ndarray):
+        frames = torch.from_numpy(np.ascontiguousarray(frames, dtype=np.uint8))
+    if not frames.is_cuda:
+        frames = frames.to(device.require_cuda())
+    return device.integral_histogram(frames, spec.table, spec.bins, bin_range=bin_range,
+                                     kernel=kernel)

@@ -1,0 +1,330 @@
+// ih_capi.cu -- the extern "C" boundary (include/inthist_b200.h).
+//
+// Host-side planning, validation (reference exception order) and launches.
+// Unity build: the kernel translation units are included here so the shared
+// library is a single nvcc invocation.
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+
+#include "../../include/inthist_b200.h"
+#include "ih_kernels.cuh"
+#include "ih_queries.cu"
+#include "ih_single_pass.cu"
+
+namespace {
+
+thread_local char g_last_error[512] = "";
+
+ih_status cuda_fail(const char* where) {
+  cudaError_t e = cudaGetLastError();
+  snprintf(g_last_error, sizeof g_last_error, "%s: %s", where, cudaGetErrorString(e));
+  return IH_ERR_CUDA;
+}
+
+ih_status fail(ih_status s, const char* msg) {
+  snprintf(g_last_error, sizeof g_last_error, "%s", msg);
+  return s;
+}
+
+int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return strtoll(v, nullptr, 10);
+}
+
+constexpr int kNumSMs = 148;
+
+// ------------------------------------------------------------------ planning
+struct K2Plan {
+  int cpl = 0;       // chunks per lane; 0 = width unsupported by K2
+  int nwarps = 0;    // warps per CTA
+  int R = 4;         // rows per barrier batch
+  int ngroups = 0;   // bin groups of 4
+  int nbp = 0;       // padded slab bins
+  int nseg = 1;      // row segments per frame
+  int S = 0;         // rows per segment
+  int64_t Wp = 0;    // padded width = nwarps * cpl * 128
+};
+
+K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb) {
+  K2Plan p;
+  const int64_t nchunks = (W + ih::kChunk - 1) / ih::kChunk;
+  // at most 16 warps per CTA (<= 128 registers per thread, no spills)
+  if (nchunks <= 16) p.cpl = 1;
+  else if (nchunks <= 32) p.cpl = 2;
+  else if (nchunks <= 64) p.cpl = 4;
+  else return p;  // cpl = 0: use the cross-weave kernels
+  p.nwarps = (int)((nchunks + p.cpl - 1) / p.cpl);
+  p.Wp = (int64_t)p.nwarps * p.cpl * ih::kChunk;
+  p.R = p.cpl == 1 ? 4 : p.cpl == 2 ? 2 : 1;
+  const int64_t r_env = env_int("IH_ROWS_PER_BATCH", 0);
+  if (r_env == 1 || r_env == 2 || r_env == 4) p.R = (int)r_env;
+  p.ngroups = (nb + ih::kGroup - 1) / ih::kGroup;
+  p.nbp = p.ngroups * ih::kGroup;
+  // Enough warps in flight to saturate HBM writes; split rows into segments
+  // only when frames x groups alone do not provide them (each extra segment
+  // costs a colcounts/colprefix table of 1/S of the output, mostly in L2).
+  const int64_t target = env_int("IH_TARGET_WARPS", (int64_t)kNumSMs * 24);
+  const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", 48);
+  const int64_t base = frames * p.ngroups * p.nwarps;
+  int64_t nseg = (target + base - 1) / base;
+  const int64_t max_seg = (H + min_rows - 1) / min_rows;
+  if (nseg > max_seg) nseg = max_seg;
+  if (nseg > 65535) nseg = 65535;
+  if (nseg < 1) nseg = 1;
+  const int64_t forced = env_int("IH_NSEG", 0);
+  if (forced > 0) nseg = forced < H ? forced : H;
+  p.S = (int)((H + nseg - 1) / nseg);
+  p.nseg = (int)((H + p.S - 1) / p.S);
+  return p;
+}
+
+int resolve_kernel(int kernel, const K2Plan& p) {
+  if (kernel == IH_KERNEL_AUTO) return p.cpl ? IH_KERNEL_SINGLE_PASS : IH_KERNEL_CROSSWEAVE;
+  return kernel;
+}
+
+size_t k2_ws_bytes(int64_t frames, const K2Plan& p) {
+  if (p.nseg <= 1) return 0;
+  return (size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint32_t);
+}
+
+struct Call {
+  const uint8_t* img;
+  int64_t frames, H, W, pitch, fstride;
+  ih::RelLut lut;
+  int nb;
+  int kernel;
+  K2Plan plan;
+  cudaStream_t stream;
+};
+
+// Validation in the reference's order: shape (core.py:28-36, :72-79),
+// capacity (core.py:53-57), then parameters.
+ih_status validate(const uint8_t* img, int64_t frames, int64_t H, int64_t W, int64_t pitch,
+                   int64_t fstride, const uint8_t* lut256, int32_t bins, int32_t bin_lo,
+                   int32_t bin_hi, int32_t kernel, Call* c) {
+  if (frames < 1 || H < 1 || W < 1) return fail(IH_ERR_SHAPE, "image must be a non-empty 2D array");
+  if (bins < 1 || bins > 256) return fail(IH_ERR_SHAPE, "bin count must be in [1, 256]");
+  if (!lut256) return fail(IH_ERR_SHAPE, "lookup table must have exactly 256 entries");
+  for (int v = 0; v < 256; ++v)
+    if (lut256[v] >= bins) return fail(IH_ERR_SHAPE, "lookup table entries must lie in [0, bins)");
+  if (bin_lo < 0 || bin_hi > bins || bin_lo >= bin_hi)
+    return fail(IH_ERR_SHAPE, "bin slab must satisfy 0 <= bin_lo < bin_hi <= bins");
+  if ((uint64_t)W * (uint64_t)H > 0xffffffffull)
+    return fail(IH_ERR_CAPACITY, "image exceeds the 32-bit count range");
+  if (!img) return fail(IH_ERR_PARAM, "null image pointer");
+  if (pitch < W) return fail(IH_ERR_PARAM, "img_pitch < width");
+  if (frames > 1 && fstride < H * pitch) return fail(IH_ERR_PARAM, "frame_stride < height*img_pitch");
+  if (frames > 65535) return fail(IH_ERR_PARAM, "at most 65535 frames per call");
+  if (kernel < IH_KERNEL_AUTO || kernel > IH_KERNEL_CROSSWEAVE)
+    return fail(IH_ERR_PARAM, "unknown kernel");
+  c->img = img;
+  c->frames = frames;
+  c->H = H;
+  c->W = W;
+  c->pitch = pitch;
+  c->fstride = frames > 1 ? fstride : H * pitch;
+  c->nb = bin_hi - bin_lo;
+  for (int v = 0; v < 256; ++v) {
+    const int rel = (int)lut256[v] - bin_lo;
+    c->lut.rel[v] = (rel >= 0 && rel < c->nb) ? (uint8_t)rel : (uint8_t)0xff;
+  }
+  c->plan = plan_k2(frames, H, W, c->nb);
+  c->kernel = resolve_kernel(kernel, c->plan);
+  if (c->kernel == IH_KERNEL_SINGLE_PASS && c->plan.cpl == 0)
+    return fail(IH_ERR_PARAM, "single-pass kernel supports width <= 8192; use crossweave");
+  return IH_OK;
+}
+
+bool aligned_rows(const Call& c) {
+  return ((uintptr_t)c.img % 4 == 0) && (c.pitch % 4 == 0) && (c.fstride % 4 == 0);
+}
+
+ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
+  if (c.kernel != IH_KERNEL_SINGLE_PASS || c.plan.nseg <= 1) return IH_OK;
+  const K2Plan& p = c.plan;
+  if (ws_bytes < k2_ws_bytes(c.frames, p) || !ws)
+    return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
+  const int nslab64 = (p.nbp + 63) / 64;
+  dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1),
+            (unsigned)(c.frames * nslab64));
+  ih::k2_colcounts<<<grid, 128, 0, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S,
+                                                p.nseg, p.nbp, p.Wp, nslab64, (uint32_t*)ws);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts");
+  const int64_t total = c.frames * p.nbp * p.Wp;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+  ih::k2_colprefix<<<(unsigned)blocks, 256, 0, c.stream>>>((uint32_t*)ws, c.frames, p.nseg, p.nbp,
+                                                           p.Wp);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colprefix");
+  return IH_OK;
+}
+
+template <int CPL, int R>
+ih_status launch_k2_cr(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads) {
+  const bool vec = (c.W % 4) == 0;
+  const bool al = aligned_rows(c);
+  if (vec && al) ih::k2_scan<CPL, R, true, true><<<grid, threads, 0, c.stream>>>(a, c.lut);
+  else if (vec) ih::k2_scan<CPL, R, true, false><<<grid, threads, 0, c.stream>>>(a, c.lut);
+  else if (al) ih::k2_scan<CPL, R, false, true><<<grid, threads, 0, c.stream>>>(a, c.lut);
+  else ih::k2_scan<CPL, R, false, false><<<grid, threads, 0, c.stream>>>(a, c.lut);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_scan");
+  return IH_OK;
+}
+
+ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
+  if (!out) return fail(IH_ERR_PARAM, "null output pointer");
+  if (c.kernel == IH_KERNEL_CROSSWEAVE) {
+    const int ngroups = (c.nb + ih::kGroup - 1) / ih::kGroup;
+    dim3 grid((unsigned)ngroups, (unsigned)((c.H + 7) / 8), (unsigned)c.frames);
+    if (grid.y > 65535) return fail(IH_ERR_PARAM, "crossweave kernel supports height <= 524280");
+    const bool vec = (c.W % 4) == 0, al = aligned_rows(c);
+    if (vec && al) ih::k1_rowscan<true, true><<<grid, 256, 0, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.nb, c.lut, out);
+    else if (vec) ih::k1_rowscan<true, false><<<grid, 256, 0, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.nb, c.lut, out);
+    else if (al) ih::k1_rowscan<false, true><<<grid, 256, 0, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.nb, c.lut, out);
+    else ih::k1_rowscan<false, false><<<grid, 256, 0, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.nb, c.lut, out);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k1_rowscan");
+    const int64_t planes = c.frames * c.nb;
+    const int64_t per = vec ? c.W / 4 : c.W;
+    int64_t blocks = (planes * per + 255) / 256;
+    if (blocks > kNumSMs * 32) blocks = kNumSMs * 32;
+    if (c.H > 1) {
+      if (vec) ih::k1b_colscan<true><<<(unsigned)blocks, 256, 0, c.stream>>>(out, planes, c.H, c.W);
+      else ih::k1b_colscan<false><<<(unsigned)blocks, 256, 0, c.stream>>>(out, planes, c.H, c.W);
+      if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k1b_colscan");
+    }
+    return IH_OK;
+  }
+  const K2Plan& p = c.plan;
+  if (p.nseg > 1 && (ws_bytes < k2_ws_bytes(c.frames, p) || !ws))
+    return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
+  ih::ScanArgs a;
+  a.img = c.img;
+  a.H = c.H;
+  a.W = c.W;
+  a.pitch = c.pitch;
+  a.fstride = c.fstride;
+  a.nb = c.nb;
+  a.nbp = p.nbp;
+  a.S = p.S;
+  a.nseg = p.nseg;
+  a.Wp = p.Wp;
+  a.colpre = p.nseg > 1 ? (const uint32_t*)ws : nullptr;
+  a.out = out;
+  dim3 grid((unsigned)p.ngroups, (unsigned)p.nseg, (unsigned)c.frames);
+  const int threads = p.nwarps * 32;
+  switch (p.cpl * 10 + p.R) {
+    case 14: return launch_k2_cr<1, 4>(c, a, grid, threads);
+    case 12: return launch_k2_cr<1, 2>(c, a, grid, threads);
+    case 24: return launch_k2_cr<2, 4>(c, a, grid, threads);
+    case 22: return launch_k2_cr<2, 2>(c, a, grid, threads);
+    case 11: return launch_k2_cr<1, 1>(c, a, grid, threads);
+    case 21: return launch_k2_cr<2, 1>(c, a, grid, threads);
+    case 42: return launch_k2_cr<4, 2>(c, a, grid, threads);
+    case 41: return launch_k2_cr<4, 1>(c, a, grid, threads);
+    default: return fail(IH_ERR_PARAM, "internal: no K2 instantiation for plan");
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
+                          int32_t kernel) {
+  if (frames < 1 || height < 1 || width < 1 || slab_bins < 1) return 0;
+  K2Plan p = plan_k2(frames, height, width, slab_bins);
+  if (resolve_kernel(kernel, p) != IH_KERNEL_SINGLE_PASS || p.cpl == 0) return 0;
+  return k2_ws_bytes(frames, p);
+}
+
+ih_status ih_ih_prepare(const uint8_t* img, int64_t frames, int64_t height, int64_t width,
+                        int64_t img_pitch, int64_t frame_stride, const uint8_t* lut256,
+                        int32_t bins, int32_t bin_lo, int32_t bin_hi, void* workspace,
+                        size_t workspace_bytes, int32_t kernel, void* stream) {
+  Call c;
+  ih_status st = validate(img, frames, height, width, img_pitch, frame_stride, lut256, bins,
+                          bin_lo, bin_hi, kernel, &c);
+  if (st != IH_OK) return st;
+  c.stream = (cudaStream_t)stream;
+  return launch_prepare(c, workspace, workspace_bytes);
+}
+
+ih_status ih_ih_scan(const uint8_t* img, int64_t frames, int64_t height, int64_t width,
+                     int64_t img_pitch, int64_t frame_stride, const uint8_t* lut256, int32_t bins,
+                     int32_t bin_lo, int32_t bin_hi, uint32_t* out, void* workspace,
+                     size_t workspace_bytes, int32_t kernel, void* stream) {
+  Call c;
+  ih_status st = validate(img, frames, height, width, img_pitch, frame_stride, lut256, bins,
+                          bin_lo, bin_hi, kernel, &c);
+  if (st != IH_OK) return st;
+  c.stream = (cudaStream_t)stream;
+  return launch_scan(c, out, workspace, workspace_bytes);
+}
+
+ih_status ih_integral_histogram(const uint8_t* img, int64_t frames, int64_t height, int64_t width,
+                                int64_t img_pitch, int64_t frame_stride, const uint8_t* lut256,
+                                int32_t bins, int32_t bin_lo, int32_t bin_hi, uint32_t* out,
+                                void* workspace, size_t workspace_bytes, int32_t kernel,
+                                void* stream) {
+  Call c;
+  ih_status st = validate(img, frames, height, width, img_pitch, frame_stride, lut256, bins,
+                          bin_lo, bin_hi, kernel, &c);
+  if (st != IH_OK) return st;
+  c.stream = (cudaStream_t)stream;
+  st = launch_prepare(c, workspace, workspace_bytes);
+  if (st != IH_OK) return st;
+  return launch_scan(c, out, workspace, workspace_bytes);
+}
+
+ih_status ih_region_histograms(const uint32_t* t, int32_t nb, int64_t height, int64_t width,
+                               const int32_t* regions, int64_t q, uint64_t* out, void* stream) {
+  if (nb < 1 || height < 1 || width < 1) return fail(IH_ERR_SHAPE, "tensor must be non-empty");
+  if (q < 0) return fail(IH_ERR_PARAM, "negative query count");
+  if (q == 0) return IH_OK;
+  if (!t || !regions || !out) return fail(IH_ERR_PARAM, "null pointer");
+  if ((uintptr_t)regions % 16 != 0) return fail(IH_ERR_PARAM, "regions must be 16-byte aligned");
+  const int64_t total = q * nb;
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > kNumSMs * 32) blocks = kNumSMs * 32;
+  ih::k3_region_histograms<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      t, nb, height, width, reinterpret_cast<const int4*>(regions), q,
+      reinterpret_cast<unsigned long long*>(out));
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k3_region_histograms");
+  return IH_OK;
+}
+
+ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_t width, int32_t h,
+                           int32_t w, int64_t* out, void* stream) {
+  if (h < 1 || w < 1) return fail(IH_ERR_PARAM, "window extents must be >= 1");
+  if (h > height || w > width) return fail(IH_ERR_BOUNDS, "window exceeds image");
+  if (nb < 1) return fail(IH_ERR_SHAPE, "tensor must be non-empty");
+  if (!t || !out) return fail(IH_ERR_PARAM, "null pointer");
+  const int64_t total = (int64_t)nb * (height - h + 1) * (width - w + 1);
+  int64_t blocks = (total + 255) / 256;
+  if (blocks > kNumSMs * 32) blocks = kNumSMs * 32;
+  ih::k4_window_counts<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+      t, nb, height, width, h, w, reinterpret_cast<long long*>(out));
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts");
+  return IH_OK;
+}
+
+const char* ih_status_string(ih_status s) {
+  switch (s) {
+    case IH_OK: return "IH_OK";
+    case IH_ERR_SHAPE: return "IH_ERR_SHAPE";
+    case IH_ERR_CAPACITY: return "IH_ERR_CAPACITY";
+    case IH_ERR_PARAM: return "IH_ERR_PARAM";
+    case IH_ERR_BOUNDS: return "IH_ERR_BOUNDS";
+    case IH_ERR_CUDA: return "IH_ERR_CUDA";
+  }
+  return "IH_ERR_UNKNOWN";
+}
+
+const char* ih_last_error(void) { return g_last_error; }
+
+int32_t ih_abi_version(void) { return (1 << 16) | 0; }
+
+}  // extern "C"

@@ -1,0 +1,91 @@
+// ih_kernels.cuh -- sm_100a kernels of the B200 integral-histogram engine.
+//
+// Reference algorithm (pkg/src/inthist/, read-only reference):
+//   H_b(r,c) = #{ (r',c') : r'<=r, c'<=c, Q(I(r',c')) = b }    (core.py:1-7, :106-128)
+// computed by the reference with four CPU strategies (strategies.py:86-229).
+// All kernels below produce the identical bin-major (B,H,W) uint32 tensor.
+//
+// Notation used throughout:
+//   chunk   = 128 consecutive columns = one warp-wide row piece, 4 pixels/lane
+//   group   = 4 consecutive bins of the slab, packed one byte per bin in a u32
+//   segment = S consecutive rows handled by one CTA of the single-pass kernel
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ih {
+
+constexpr int kChunk = 128;       // columns per warp chunk
+constexpr int kGroup = 4;         // bins per packed group
+constexpr unsigned kFull = 0xffffffffu;
+
+// Per-call binning table: relative bin (lut[v] - bin_lo) or 0xFF when the
+// bin lies outside the slab [bin_lo, bin_hi).  Passed by value (kernel param).
+struct RelLut {
+  uint8_t rel[256];
+};
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ uint32_t byte_of(uint32_t v, int i) {
+  return __byte_perm(v, 0u, 0x4440u | (uint32_t)i);
+}
+
+// Inclusive warp scan; with packed operands every byte lane scans
+// independently as long as no byte exceeds 255 (callers guarantee <=128).
+__device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(kFull, x, d);
+    if (lane >= d) x += y;
+  }
+  return x;
+}
+
+// Streaming (evict-first) 16-byte / 4-byte global stores: every output byte
+// is written exactly once and never re-read by the producing kernel.
+__device__ __forceinline__ void st_stream_v4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c,
+                                             uint32_t d) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
+               "r"(d)
+               : "memory");
+}
+__device__ __forceinline__ void st_stream(uint32_t* p, uint32_t a) {
+  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+}
+
+// Build the packed one-hot table of one bin group in shared memory:
+// oh[v] = 1 << 8*(rel(v) - 4g) when rel(v) is in the group, else 0;
+// oh[256] = 0 is the "column beyond the image edge" entry.
+__device__ __forceinline__ void build_onehot(uint32_t* oh, const RelLut& lut, int g) {
+  for (int v = threadIdx.x; v < 257; v += blockDim.x) {
+    uint32_t word = 0;
+    if (v < 256) {
+      uint32_t d = (uint32_t)lut.rel[v] - (uint32_t)(g * kGroup);
+      if (d < (uint32_t)kGroup) word = 1u << (8u * d);
+    }
+    oh[v] = word;
+  }
+}
+
+// Load the 4 pixels of one lane in one chunk row and return their 4 one-hot
+// words through the table.  `inval` has bit 8 set for pixel slots at or
+// beyond the right image edge (they map to oh[256] == 0).
+template <bool ALIGNED>
+__device__ __forceinline__ void load_onehot4(const uint8_t* row, int64_t c, int64_t W,
+                                             const uint32_t* oh, const uint32_t inval[4],
+                                             uint32_t out[4]) {
+  uint32_t px = 0;
+  if (c < W) {
+    if (ALIGNED) {
+      px = __ldg(reinterpret_cast<const uint32_t*>(row + c));
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (c + j < W) px |= (uint32_t)__ldg(row + c + j) << (8 * j);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) out[j] = oh[((px >> (8 * j)) & 0xffu) | inval[j]];
+}
+
+}  // namespace ih

@@ -1,0 +1,219 @@
+"""Device-resident API over the C ABI: torch CUDA tensors in, torch tensors out.
+
+PyTorch is plumbing here (device memory, streams); every computation is one
+of the sm_100a kernels behind include/inthist_b200.h.  All calls are
+stream-ordered on the current torch stream of the tensor's device and do not
+synchronise the host.
+
+    t = integral_histogram(frames_u8, table, bins)            # (F, B, H, W) uint32
+    q = region_histograms(t[0], regions_int32)                # (Q, B) uint64
+    w = window_counts(t[0], h, w)                             # (B, H-h+1, W-w+1) int64
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from . import _native
+from .errors import BoundsError, DeviceError, ParameterError, ShapeError
+
+_workspaces: dict[int, torch.Tensor] = {}
+
+
+def require_cuda(device=None) -> torch.device:
+    if not torch.cuda.is_available():
+        raise DeviceError("no CUDA device visible: the B200 engine has no CPU fallback")
+    _native.lib()
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    if dev.type != "cuda":
+        raise DeviceError(f"expected a CUDA device, got {dev}")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def _stream_handle(dev: torch.device, stream=None) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream(dev)
+    return int(s.cuda_stream)
+
+
+def workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
+    """Per-device scratch buffer, grown on demand (caller-owned per the ABI)."""
+    idx = dev.index
+    ws = _workspaces.get(idx)
+    if ws is None or ws.numel() < nbytes:
+        ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
+        _workspaces[idx] = ws
+    return ws
+
+
+def _lut_array(table) -> np.ndarray:
+    lut = np.ascontiguousarray(np.asarray(table), dtype=np.uint8)
+    if lut.shape != (256,):
+        raise ShapeError("lookup table must have exactly 256 entries")
+    return lut
+
+
+def _frames_view(images: torch.Tensor):
+    if not isinstance(images, torch.Tensor):
+        raise ShapeError("images must be a torch tensor")
+    if images.dtype != torch.uint8:
+        raise ShapeError(f"image dtype must be uint8, got {images.dtype}")
+    if images.dim() == 2:
+        images = images.unsqueeze(0)
+    if images.dim() != 3 or images.numel() == 0:
+        raise ShapeError("images must be a non-empty (H, W) or (F, H, W) tensor")
+    if images.stride(-1) != 1:
+        images = images.contiguous()
+    return images
+
+
+class _Args:
+    __slots__ = ("images", "frames", "H", "W", "pitch", "fstride", "lut", "bins", "lo", "hi",
+                 "kernel", "dev", "stream")
+
+
+def _prepare_args(images, table, bins, bin_range, kernel, stream) -> _Args:
+    imgs = _frames_view(images)
+    dev = require_cuda(imgs.device)
+    a = _Args()
+    a.images = imgs
+    a.frames, a.H, a.W = (int(x) for x in imgs.shape)
+    a.pitch = int(imgs.stride(1))
+    a.fstride = int(imgs.stride(0)) if a.frames > 1 else a.H * a.pitch
+    a.lut = _lut_array(table)
+    a.bins = int(bins)
+    a.lo, a.hi = (0, a.bins) if bin_range is None else (int(bin_range[0]), int(bin_range[1]))
+    if kernel not in _native.KERNELS:
+        raise ParameterError(f"unknown kernel {kernel!r}; expected one of {sorted(_native.KERNELS)}")
+    a.kernel = _native.KERNELS[kernel]
+    a.dev = dev
+    a.stream = _stream_handle(dev, stream)
+    return a
+
+
+def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto") -> int:
+    return int(_native.lib().ih_workspace_bytes(frames, height, width, slab_bins,
+                                                _native.KERNELS[kernel]))
+
+
+def empty_output(frames: int, slab_bins: int, height: int, width: int, device) -> torch.Tensor:
+    return torch.empty((frames, slab_bins, height, width), dtype=torch.uint32, device=device)
+
+
+def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, out=None,
+                       kernel: str = "auto", stream=None) -> torch.Tensor:
+    """Integral histograms of (F, H, W) or (H, W) uint8 CUDA frames.
+
+    Returns (F, hi-lo, H, W) torch.uint32 (or (hi-lo, H, W) for a 2D input):
+    the bin-major tensor of IntegralHistogram.counts (core.py:106-116) for the
+    bins [lo, hi) of ``bin_range`` (default: all).  Bit-identical to every
+    reference strategy (strategies.py:109-229).
+    """
+    squeeze = images.dim() == 2
+    a = _prepare_args(images, table, bins, bin_range, kernel, stream)
+    nb = a.hi - a.lo
+    if nb < 1 or a.lo < 0 or a.hi > a.bins:
+        raise ShapeError("bin slab must satisfy 0 <= lo < hi <= bins")
+    if out is None:
+        out = empty_output(a.frames, nb, a.H, a.W, a.dev)
+    else:
+        if out.dtype not in (torch.uint32, torch.int32) or not out.is_contiguous():
+            raise ShapeError("out must be a contiguous uint32 tensor")
+        if out.numel() != a.frames * nb * a.H * a.W or out.device != a.dev:
+            raise ShapeError("out has the wrong size or device")
+    ws_n = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, nb, a.kernel)
+    ws = workspace(a.dev, ws_n)
+    L = _native.lib()
+    _native.check(L.ih_integral_histogram(
+        a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel(), a.kernel, a.stream))
+    if squeeze and out.dim() == 4:
+        return out[0]
+    return out
+
+
+def prepare(images, table, bins, bin_range=None, kernel="auto", stream=None) -> None:
+    """Phase 1 of integral_histogram (segment carries), for per-kernel timing."""
+    a = _prepare_args(images, table, bins, bin_range, kernel, stream)
+    ws_n = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, a.hi - a.lo, a.kernel)
+    ws = workspace(a.dev, ws_n)
+    _native.check(_native.lib().ih_ih_prepare(
+        a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+        a.bins, a.lo, a.hi, ws.data_ptr(), ws.numel(), a.kernel, a.stream))
+
+
+def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None) -> torch.Tensor:
+    """Phase 2 of integral_histogram (the dominant single-pass kernel)."""
+    a = _prepare_args(images, table, bins, bin_range, kernel, stream)
+    ws_n = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, a.hi - a.lo, a.kernel)
+    ws = workspace(a.dev, ws_n)
+    _native.check(_native.lib().ih_ih_scan(
+        a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel(), a.kernel, a.stream))
+    return out
+
+
+def _check_tensor(t: torch.Tensor) -> torch.Tensor:
+    if t.dim() != 3 or t.dtype not in (torch.uint32, torch.int32):
+        raise ShapeError("tensor must be a 3D uint32 array (bins, height, width)")
+    if not t.is_cuda:
+        raise DeviceError("integral-histogram tensor must live on a CUDA device")
+    return t.contiguous()
+
+
+def region_histograms(t: torch.Tensor, regions, stream=None) -> torch.Tensor:
+    """Batched core.py:179-195: (Q, 4) inclusive (r0,c0,r1,c1) -> (Q, nb) uint64.
+
+    Validation follows core.py:142 (degenerate) then core.py:158 (outside),
+    done on the host before launch when ``regions`` is host data.
+    """
+    t = _check_tensor(t)
+    nb, H, W = (int(x) for x in t.shape)
+    if isinstance(regions, torch.Tensor) and regions.is_cuda:
+        regs = regions.to(torch.int32).contiguous().view(-1, 4)
+    else:
+        r = np.ascontiguousarray(np.asarray(regions, dtype=np.int64).reshape(-1, 4))
+        if r.size:
+            if ((r[:, 0] < 0) | (r[:, 1] < 0) | (r[:, 0] > r[:, 2]) | (r[:, 1] > r[:, 3])).any():
+                raise BoundsError("degenerate region")
+            if ((r[:, 2] >= H) | (r[:, 3] >= W)).any():
+                raise BoundsError(f"region outside {W}x{H} image")
+        regs = torch.from_numpy(r.astype(np.int32)).to(t.device)
+    Q = int(regs.shape[0])
+    out = torch.empty((Q, nb), dtype=torch.uint64, device=t.device)
+    if Q:
+        _native.check(_native.lib().ih_region_histograms(
+            t.data_ptr(), nb, H, W, regs.data_ptr(), Q, out.data_ptr(),
+            _stream_handle(t.device, stream)))
+    return out
+
+
+def window_counts(t: torch.Tensor, h: int, w: int, stream=None) -> torch.Tensor:
+    """likelihood.py:34-52 on the device -> (nb, H-h+1, W-w+1) int64."""
+    if h < 1 or w < 1:
+        raise ParameterError("window extents must be >= 1")
+    t = _check_tensor(t)
+    nb, H, W = (int(x) for x in t.shape)
+    if h > H or w > W:
+        raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
+    out = torch.empty((nb, H - h + 1, W - w + 1), dtype=torch.int64, device=t.device)
+    _native.check(_native.lib().ih_window_counts(
+        t.data_ptr(), nb, H, W, int(h), int(w), out.data_ptr(), _stream_handle(t.device, stream)))
+    return out
+
+
+def upload_image(pixels: np.ndarray, device=None) -> torch.Tensor:
+    """H2D of a host (H, W) uint8 image into a 16-byte-pitched device buffer
+    (aligned 32-bit pixel loads in the kernels for every width).  Returns the
+    (H, W) view."""
+    dev = require_cuda(device)
+    px = np.ascontiguousarray(pixels, dtype=np.uint8)
+    H, W = px.shape
+    if W % 16 == 0:
+        return torch.from_numpy(px).to(dev)
+    pitch = (W + 15) // 16 * 16
+    buf = torch.empty((H, pitch), dtype=torch.uint8, device=dev)
+    buf[:, :W].copy_(torch.from_numpy(px))
+    return buf[:, :W]

@@ -1,0 +1,165 @@
+"""Generate the golden fixtures by running the REFERENCE `inthist` package.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the reference from /root/reference/pkg/src and writes small
+fixtures next to this script.  They pin both the oracle (oracle/) and the
+CUDA path to the reference's own outputs.  Nothing on the GPU box reads
+/root/reference; only these committed files travel.
+
+Fixtures:
+  c1_instances.json   -- the 200 acceptance-C1 instances (test_acceptance.py:48-61,
+                         seed 20260823): (W, H, B, tile), crc32 of the image bytes
+                         and crc32 of the reference compute_sequential tensor.
+  configs.json        -- tensor_checksum (bench.py:65-66) of the BASELINE configs
+                         (synth_image seed 0; HD frames seeds 0..63), computed here
+                         with the reference; the 8192x8192x256 per-plane values are
+                         SURVEY.md Appendix A (reference compute_streamed, 698 s).
+  small_cases.npz     -- full reference tensors for hand-picked edge cases
+                         (known answers of tests/test_strategies.py, explicit LUTs,
+                         B=256, ragged shapes), plus reference region_histogram
+                         and window_counts outputs on them.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+import sys
+import zlib
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REF)
+
+import inthist  # noqa: E402  (the reference)
+from inthist.bench import synth_image, tensor_checksum  # noqa: E402
+from inthist.likelihood import window_counts  # noqa: E402
+
+SEED = 20260823
+WIDTHS = [1, 2, 3, 5, 17, 33, 64, 97, 131, 257]
+HEIGHTS = [1, 2, 7, 19, 33, 61, 96, 128, 193]
+BINS = [1, 2, 3, 16, 64]
+TILES = [1, 7, 64]
+
+
+def c1_instances():
+    """test_acceptance.py:48-61 + :68-75 (same RNG stream, same order)."""
+    rng = np.random.default_rng(SEED)
+    fixed = [(1, 1, 1, 1), (1, 1, 64, 64), (257, 193, 16, 64), (257, 193, 64, 7)]
+    inst = list(fixed)
+    while len(inst) < 200:
+        inst.append((int(rng.choice(WIDTHS)), int(rng.choice(HEIGHTS)),
+                     int(rng.choice(BINS)), int(rng.choice(TILES))))
+    out = []
+    for w, h, b, tile in inst:
+        px = rng.integers(0, 256, size=(h, w), dtype=np.uint8)
+        ih = inthist.compute_sequential(inthist.GrayImage(px), inthist.BinSpec.uniform(b))
+        out.append({"w": w, "h": h, "bins": b, "tile": tile,
+                    "img_crc": f"{zlib.crc32(px.tobytes()):08x}",
+                    "crc": tensor_checksum(ih)})
+    return out
+
+
+def configs():
+    res = {}
+    for (w, h, b) in [(64, 64, 16), (512, 512, 32), (1920, 1080, 32), (3840, 2160, 128)]:
+        img = synth_image(w, h, 0)
+        ih = inthist.compute(img, inthist.BinSpec.uniform(b), inthist.CROSSWEAVE)
+        res[f"{w}x{h}x{b}"] = {"seed": 0, "crc": tensor_checksum(ih),
+                              "img_crc": f"{zlib.crc32(img.pixels.tobytes()):08x}"}
+        print(w, h, b, res[f"{w}x{h}x{b}"], flush=True)
+    spec = inthist.BinSpec.uniform(32)
+    frames = []
+    for k in range(64):
+        ih = inthist.compute(synth_image(1920, 1080, k), spec, inthist.CROSSWEAVE)
+        frames.append(tensor_checksum(ih))
+    res["1920x1080x32_frames"] = frames
+    res["8192x8192x256"] = {
+        "seed": 0,
+        "source": "SURVEY.md Appendix A (reference compute_streamed, 1-bin chunks)",
+        "crc": "b416da31",
+        "plane_crc": APPENDIX_A_PLANES.split(),
+    }
+    return res
+
+
+APPENDIX_A_PLANES = """
+a4def62a 92b94c39 4f2dfcbd 02d3fa73 a3df4740 88d08cdc 34a3d251 ee8209e6 64e6892a fc66f578 c4c1f941 a05a472b b163325e 14df6051 a5e8704c 163f14b7
+98c6ee77 afa8e8cb 37f3da33 0d434b37 b3d41091 fb9275ac e5fd589e 17506c2f d4551290 dbd8b564 aff7b50e 1de79817 2919dacd 78f42ceb 17131024 995c6c4e
+deef505b 55ed3d38 96cef745 2940c5e1 16701882 3be29c06 ba9f589a 82fbdaac 1df331f2 d1323d11 83702f8d 6791ac60 1fe89d79 0c3e7556 c24abf27 405fd665
+b166b92a 0affe75c 5945318d bbb9139e 0d1e95cc 4ffff944 572635db d4e778e4 4424e688 42914ee5 89afd8af 0f66b69d df777d4c 7f7ac588 65f4773a 1115e97d
+3fb6b639 c5a2d82c 61bfa510 88144127 20044f27 4694cf27 0dae07c5 7835eea1 f53bd16b 8838ef20 b48559f7 f9a4c1c2 a0def3d4 4d01a1db aa2eb3be c9980e60
+b5659310 849380da 09fd7e2e 371b1d40 f9776323 f59595cc e7ec2568 d503ec9d f43d3b96 0600d24e 437bdeda 5baf07b6 453923ab ffcf3919 f0987739 1d0b6b41
+394a4216 9cf019c0 130b81f9 7359ccbf bd91e427 862b0a4f e1faa447 a7838aa2 499cf937 239d5e3f 2e664cc2 6be24750 09525504 3bff17c8 c076bea6 b36bcce7
+abb8066e 21a20e17 8dbc9aa2 4c6f645e 36a86a31 a72a3b4b 72043292 4e3431a3 bc7f6318 a8755037 d95b8ad5 39ab25ea 6a9e874f 6110048a 5ce43972 a08408ae
+555c1a94 7756a7e2 beeffce2 e0045645 7ec4a974 ec45fe5c 873a2ac3 92a0c57f 81740d8c e06034c8 afb5b588 b2a3dee0 6eb56f1e 99f60d4e 32256cc9 c111de02
+424f9801 b815ff5e 1ea8c973 8714f7f0 a6593702 88713c7e a8a16769 914e9d1b c3318969 ceb9f1b1 2c1759bc 0b7b5a20 7ec4e3a4 ba35bb1a 5994f301 5cc564e4
+b7383b01 afba2789 982ec5bc 0d01df62 9d8a3ba2 f2d7bdba 7cd26741 a36dc522 70ba2514 f3157357 a75e37a9 54e6a218 45e96fc9 164cdf97 8a958288 dfa94281
+eff1a8ab 8c765032 f8a88801 3c4f0b30 522d2dce b52be353 72d22f28 1d017ebf 621d6bc7 1b7514a4 1885ba25 01a65450 e431a76f fe187c8a 50e17df6 37b58fa6
+b2a9d636 9f10e133 f7a66308 2efb49cd eaf095cf edd4f439 1f9b0802 d0a55af7 362a88ce f59ad5b7 bc8e9c60 5e8a049d ab57542b 1180463c 9de4e442 1e200deb
+07356ead 5da65d4f 3d0b0cc6 eb78fdac f673acdc 4daa2ac3 b6c7c826 7ff3bd99 dac93f98 b285cfcf 8f9808be 65c9ea2f 144074c8 3729789e 26d07300 614b6e0e
+4f3ac100 e56d38b6 9b6a514e aac0672a cd56db48 b35a6ce7 6fd75e5d e00569d9 445a76a5 95d253b2 4b7ce0f4 fb6fac7b cd056aeb d6cd9fd2 5a49d98e 9b268690
+03e6ca96 232dbb23 36959ee3 4825aabf a800a1bc b0e62b0c 04e20e75 09755bf4 9fb7a34c f0f9e8a4 f7f1dca1 69a189ad 74296f72 ae1a2f8f f2be5d59 4ba6753d
+"""
+
+
+def small_cases():
+    """Edge cases with full reference tensors + query outputs."""
+    rng = np.random.default_rng(SEED + 100)
+    cases = {}
+
+    def add(name, px, spec, regions=(), windows=()):
+        ih = inthist.compute_sequential(inthist.GrayImage(px), spec)
+        cases[f"{name}__img"] = px
+        cases[f"{name}__lut"] = np.asarray(spec.table, dtype=np.uint8)
+        cases[f"{name}__bins"] = np.array(spec.bins)
+        cases[f"{name}__counts"] = ih.counts
+        if regions:
+            regs = np.array(regions, dtype=np.int32)
+            got = np.stack([inthist.region_histogram(ih, inthist.Region(*r)).counts
+                            for r in regions])
+            cases[f"{name}__regions"] = regs
+            cases[f"{name}__region_counts"] = got
+        for (h, w) in windows:
+            cases[f"{name}__win_{h}x{w}"] = window_counts(ih, h, w)
+
+    add("pix2x2", np.array([[0, 255], [128, 0]], dtype=np.uint8), inthist.BinSpec.uniform(2))
+    add("const3x5", np.full((3, 5), 200, dtype=np.uint8), inthist.BinSpec.uniform(4))
+    add("one77", np.array([[77]], dtype=np.uint8), inthist.BinSpec.uniform(16))
+    add("row1x31", rng.integers(0, 256, (1, 31), dtype=np.uint8), inthist.BinSpec.uniform(4))
+    add("col47x1", rng.integers(0, 256, (47, 1), dtype=np.uint8), inthist.BinSpec.uniform(3))
+    add("b256_64x64", rng.integers(0, 256, (64, 64), dtype=np.uint8), inthist.BinSpec.uniform(256),
+        regions=[(0, 0, 63, 63), (5, 7, 40, 33), (63, 63, 63, 63)], windows=[(8, 8)])
+    tab = rng.integers(0, 7, 256)
+    add("explicit7_97x61", rng.integers(0, 256, (61, 97), dtype=np.uint8), inthist.BinSpec.explicit(tab),
+        regions=[(0, 0, 60, 96), (3, 4, 3, 4), (10, 20, 50, 90)], windows=[(5, 4), (61, 97), (1, 1)])
+    tab2 = np.zeros(256, dtype=np.uint8)
+    tab2[128:] = 1
+    add("explicit_step_33x130", rng.integers(0, 256, (33, 130), dtype=np.uint8), inthist.BinSpec(2, tab2))
+    add("ragged_193x257x64", rng.integers(0, 256, (193, 257), dtype=np.uint8), inthist.BinSpec.uniform(64),
+        regions=[(int(a), int(b), int(c), int(d)) for a, b, c, d in
+                 [(0, 0, 192, 256), (1, 1, 1, 1), (100, 3, 150, 255), (0, 200, 0, 256)]],
+        windows=[(64, 64), (7, 13)])
+    add("wide1x600", rng.integers(0, 256, (1, 600), dtype=np.uint8), inthist.BinSpec.uniform(5))
+    return cases
+
+
+def main():
+    inst = c1_instances()
+    with open(os.path.join(HERE, "c1_instances.json"), "w") as fh:
+        json.dump(inst, fh, indent=0)
+    print("c1 done", flush=True)
+    np.savez_compressed(os.path.join(HERE, "small_cases.npz"), **small_cases())
+    print("small cases done", flush=True)
+    with open(os.path.join(HERE, "configs.json"), "w") as fh:
+        json.dump(configs(), fh, indent=1)
+    print("configs done", flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,304 @@
+"""Parity of the CUDA path against the reference (golden fixtures) and the
+oracle, bit-exact, through the C ABI.  Needs a B200: run with -m gpu."""
+
+import os
+import zlib
+
+import numpy as np
+import pytest
+
+from conftest import c1_images
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+import paper_1711_01919_b200 as ih  # noqa: E402
+from paper_1711_01919_b200 import device  # noqa: E402
+
+
+def crc_of(t) -> str:
+    a = t.cpu().numpy() if hasattr(t, "cpu") else t
+    return f"{zlib.crc32(np.ascontiguousarray(a).view(np.uint32).tobytes()):08x}"
+
+
+@pytest.fixture(autouse=True)
+def _clean_env(monkeypatch):
+    for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS"):
+        monkeypatch.delenv(k, raising=False)
+
+
+def dev_compute(px, lut, bins, kernel="auto", bin_range=None):
+    d = device.upload_image(px)
+    return device.integral_histogram(d, lut, bins, bin_range=bin_range, kernel=kernel)
+
+
+# --------------------------------------------------------------------- C1 / C7
+def test_c1_every_strategy_matches_reference(golden_c1):
+    """Acceptance C1 (test_acceptance.py:68-83): 200 seeded instances, every
+    strategy byte-identical to the reference's compute_sequential."""
+    for (w, h, b, tile, px), gold in zip(c1_images(200), golden_c1):
+        img = ih.GrayImage(px)
+        spec = ih.BinSpec.uniform(b)
+        for res in (ih.compute_sequential(img, spec), ih.compute_crossweave(img, spec),
+                    ih.compute_sts(img, spec), ih.compute_wavefront(img, spec, tile)):
+            assert crc_of(res.counts) == gold["crc"], (w, h, b, tile)
+
+
+def test_c7_worker_caps_do_not_change_output(golden_c1):
+    for (w, h, b, tile, px), gold in list(zip(c1_images(200), golden_c1))[:16]:
+        img, spec = ih.GrayImage(px), ih.BinSpec.uniform(b)
+        for workers in (1, 2, 8):
+            assert crc_of(ih.compute_crossweave(img, spec, workers).counts) == gold["crc"]
+            assert crc_of(ih.compute_wavefront(img, spec, tile, workers).counts) == gold["crc"]
+
+
+# ------------------------------------------------------------ golden small cases
+@pytest.mark.parametrize("kernel", ["auto", "single_pass", "crossweave"])
+def test_small_cases_exact(golden_small, kernel):
+    for name, case in golden_small.items():
+        px, lut, bins = case["img"], case["lut"], int(case["bins"])
+        if kernel == "single_pass" and px.shape[1] > 8192:
+            continue
+        got = dev_compute(px, lut, bins, kernel=kernel).cpu().numpy()
+        assert np.array_equal(got, case["counts"]), (name, kernel)
+
+
+def test_small_case_queries(golden_small):
+    for name, case in golden_small.items():
+        t = dev_compute(case["img"], case["lut"], int(case["bins"]))
+        if "regions" in case:
+            got = device.region_histograms(t, case["regions"]).cpu().numpy()
+            assert np.array_equal(got, case["region_counts"]), name
+        for key in case:
+            if key.startswith("win_"):
+                h, w = (int(x) for x in key[4:].split("x"))
+                got = device.window_counts(t, h, w).cpu().numpy()
+                assert np.array_equal(got, case[key]), (name, key)
+
+
+def test_known_answers():
+    img = ih.GrayImage(np.array([[0, 255], [128, 0]], dtype=np.uint8))
+    t = ih.compute_sequential(img, ih.BinSpec.uniform(2)).counts
+    assert t[0, 1, 1] == 2 and t[1, 1, 1] == 2
+    img = ih.GrayImage(np.full((3, 5), 200, dtype=np.uint8))
+    t = ih.compute_sequential(img, ih.BinSpec.uniform(4)).counts
+    hit = (200 * 4) // 256
+    assert t[hit, -1, -1] == 15 and not np.delete(t, hit, axis=0).any()
+    one = ih.GrayImage(np.array([[77]], dtype=np.uint8))
+    for s in (ih.SEQUENTIAL, ih.CROSSWEAVE, ih.SCAN_TRANSPOSE_SCAN, ih.wavefront(1)):
+        t = ih.compute(one, ih.BinSpec.uniform(16), s).counts
+        assert t.sum() == 1 and t[(77 * 16) // 256, 0, 0] == 1
+
+
+# ----------------------------------------------- kernel-internal paths vs oracle
+SHAPES = [(1, 1), (1, 193), (193, 1), (7, 131), (61, 257), (128, 128), (96, 500),
+          (300, 1030), (45, 2049), (33, 4100), (20, 8192)]
+
+
+@pytest.mark.parametrize("nseg", [0, 2, 3, 7])
+@pytest.mark.parametrize("rows_per_batch", [1, 2, 4])
+def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch):
+    """Force K2 row segmentation (colcounts/colprefix/carry-init path) and
+    every barrier batch size; compare with the oracle bit for bit."""
+    if nseg:
+        monkeypatch.setenv("IH_NSEG", str(nseg))
+    monkeypatch.setenv("IH_ROWS_PER_BATCH", str(rows_per_batch))
+    for (h, w) in SHAPES:
+        bins = int(rng.choice([1, 3, 5, 16, 64]))
+        px = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        lut = O.np_uniform_table(bins)
+        got = dev_compute(px, lut, bins, kernel="single_pass").cpu().numpy()
+        assert np.array_equal(got, O.compute_crossweave(px, lut, bins)), (h, w, bins)
+
+
+def test_auto_segmentation_sizes(rng):
+    for (h, w) in [(1080, 1920), (2160, 640), (500, 64)]:
+        for bins in (1, 4, 32):
+            px = rng.integers(0, 256, (h, w), dtype=np.uint8)
+            lut = O.np_uniform_table(bins)
+            got = dev_compute(px, lut, bins).cpu().numpy()
+            assert np.array_equal(got, O.compute_crossweave(px, lut, bins)), (h, w, bins)
+
+
+def test_unaligned_rows_and_odd_widths(rng):
+    """ALIGNED=false (odd pitch / offset) and VEC=false (W % 4 != 0) paths."""
+    for (h, w, bins) in [(37, 101, 16), (64, 255, 7), (19, 1025, 64), (5, 3, 2)]:
+        base = rng.integers(0, 256, (h, w + 7), dtype=np.uint8)
+        px = np.ascontiguousarray(base[:, 3:3 + w])
+        lut = O.np_uniform_table(bins)
+        expect = O.compute_crossweave(px, lut, bins)
+        dbase = torch.from_numpy(base).cuda()
+        view = dbase[:, 3:3 + w]  # pitch w+7, 3-byte offset
+        for kernel in ("single_pass", "crossweave"):
+            got = device.integral_histogram(view, lut, bins, kernel=kernel).cpu().numpy()
+            assert np.array_equal(got, expect), (h, w, bins, kernel)
+
+
+def test_explicit_tables_and_256_bins(rng):
+    for bins in (2, 7, 100, 256):
+        tab = rng.integers(0, bins, 256).astype(np.uint8)
+        tab[0] = bins - 1
+        spec = ih.BinSpec.explicit(tab)
+        px = rng.integers(0, 256, (77, 333), dtype=np.uint8)
+        for kernel in ("single_pass", "crossweave"):
+            got = dev_compute(px, spec.table, spec.bins, kernel=kernel).cpu().numpy()
+            assert np.array_equal(got, O.compute_crossweave(px, spec.table, spec.bins))
+
+
+def test_bin_slabs_match_slices(rng):
+    from paper_1711_01919_b200 import sharding
+
+    px = rng.integers(0, 256, (200, 700), dtype=np.uint8)
+    lut = O.np_uniform_table(37)
+    full = O.compute_crossweave(px, lut, 37)
+    for world in (2, 3, 8):
+        for lo, hi in sharding.bin_slabs(37, world):
+            if hi > lo:
+                for kernel in ("single_pass", "crossweave"):
+                    got = dev_compute(px, lut, 37, kernel=kernel, bin_range=(lo, hi))
+                    assert np.array_equal(got.cpu().numpy(), full[lo:hi]), (world, lo, hi)
+
+
+def test_frames_batch(rng):
+    frames = rng.integers(0, 256, (5, 67, 130), dtype=np.uint8)
+    lut = O.np_uniform_table(9)
+    t = ih.compute_frames(frames, ih.BinSpec.uniform(9))
+    assert t.shape == (5, 9, 67, 130)
+    for f in range(5):
+        assert np.array_equal(t[f].cpu().numpy(), O.compute_crossweave(frames[f], lut, 9))
+
+
+def test_wide_image_falls_back_to_crossweave(rng):
+    px = rng.integers(0, 256, (3, 10000), dtype=np.uint8)
+    lut = O.np_uniform_table(6)
+    got = dev_compute(px, lut, 6).cpu().numpy()
+    assert np.array_equal(got, O.compute_crossweave(px, lut, 6))
+
+
+# ------------------------------------------------------- BASELINE configs (golden)
+@pytest.mark.parametrize("key", ["64x64x16", "512x512x32", "1920x1080x32", "3840x2160x128"])
+def test_config_checksums(golden_configs, key):
+    w, h, b = (int(x) for x in key.split("x"))
+    img = O.synth_image(w, h, 0)
+    for kernel in ("auto", "crossweave"):
+        assert crc_of(dev_compute(img, O.np_uniform_table(b), b, kernel=kernel)) == \
+            golden_configs[key]["crc"], kernel
+
+
+def test_hd_64_frame_batch(golden_configs):
+    frames = np.stack([O.synth_image(1920, 1080, k) for k in range(64)])
+    t = ih.compute_frames(frames, ih.BinSpec.uniform(32))
+    torch.cuda.synchronize()
+    got = [crc_of(t[k]) for k in range(64)]
+    assert got == golden_configs["1920x1080x32_frames"]
+    # analytic invariants (acceptance C2) on the device for the whole batch
+    s = t.view(torch.int32).sum(dim=1, dtype=torch.int64)
+    rr = torch.arange(1, 1081, device=t.device)[:, None]
+    cc = torch.arange(1, 1921, device=t.device)[None, :]
+    assert bool((s == rr * cc).all())
+
+
+def test_4k_bin_sharded_slabs(golden_configs):
+    from paper_1711_01919_b200 import sharding
+
+    img = O.synth_image(3840, 2160, 0)
+    lut = O.np_uniform_table(128)
+    for world in (2, 4, 8):
+        crc = 0
+        for lo, hi in sharding.bin_slabs(128, world):
+            t = dev_compute(img, lut, 128, bin_range=(lo, hi))
+            crc = zlib.crc32(t.cpu().numpy().tobytes(), crc)
+        assert f"{crc:08x}" == golden_configs["3840x2160x128"]["crc"], world
+
+
+# ------------------------------------------------------------- queries / matching
+def test_c4_region_queries(rng):
+    """Acceptance C4 (test_acceptance.py:121-141) + batched form."""
+    for _ in range(10):
+        w, h = int(rng.integers(1, 120)), int(rng.integers(1, 90))
+        bins = int(rng.choice([1, 2, 3, 16, 64]))
+        px = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        img, spec = ih.GrayImage(px), ih.BinSpec.uniform(bins)
+        t = ih.compute_sequential(img, spec)
+        regs = []
+        for _ in range(100):
+            r0, r1 = sorted(rng.integers(0, h, 2).tolist())
+            c0, c1 = sorted(rng.integers(0, w, 2).tolist())
+            regs.append((r0, c0, r1, c1))
+        got = ih.region_histogram_batch(t, regs)
+        for k, (r0, c0, r1, c1) in enumerate(regs[:20]):
+            one = ih.region_histogram(t, ih.Region(r0, c0, r1, c1)).counts
+            assert np.array_equal(one, got[k])
+        for k, (r0, c0, r1, c1) in enumerate(regs):
+            assert np.array_equal(got[k], O.brute_region_counts(px, spec.table, bins, r0, c0, r1, c1))
+    with pytest.raises(ih.BoundsError):
+        ih.region_histogram(t, ih.Region(0, 0, h, 0))
+
+
+def test_window_counts_vs_oracle(rng):
+    px = rng.integers(0, 256, (90, 170), dtype=np.uint8)
+    lut = O.np_uniform_table(12)
+    full = O.compute_crossweave(px, lut, 12)
+    t = ih.IntegralHistogram(full)
+    for (h, w) in [(1, 1), (8, 8), (64, 64), (90, 170), (13, 1), (1, 170)]:
+        assert np.array_equal(ih.window_counts(t, h, w), O.window_counts(full, h, w)), (h, w)
+    with pytest.raises(ih.ParameterError):
+        ih.window_counts(t, 0, 3)
+    with pytest.raises(ih.BoundsError):
+        ih.window_counts(t, 91, 3)
+
+
+@pytest.mark.parametrize("metric", ["intersection", "bhattacharyya"])
+def test_likelihood_map_brute(rng, metric):
+    """Acceptance C6 (test_acceptance.py:166-190), tolerance 1e-12."""
+    px = rng.integers(0, 256, (30, 40), dtype=np.uint8)
+    img, spec = ih.GrayImage(px), ih.BinSpec.uniform(16)
+    t = ih.compute_sequential(img, spec)
+    template = ih.normalize(ih.region_histogram(t, ih.Region(10, 12, 17, 19)))
+    lmap = ih.likelihood_map(t, template, 8, 8, metric)
+    assert lmap.values.shape == (23, 33)
+    for r in range(23):
+        for c in range(33):
+            q = O.brute_region_counts(px, spec.table, 16, r, c, r + 7, c + 7).astype(np.float64) / 64
+            exp = ih.intersection(template, q) if metric == "intersection" else ih.bhattacharyya(template, q)[0]
+            assert abs(lmap.values[r, c] - exp) < 1e-12
+    assert abs(lmap.values[10, 12] - 1.0) < 1e-12
+    r, c, v = ih.best_match(lmap)
+    assert (r, c) == (10, 12) or v <= lmap.values[10, 12] + 1e-12
+
+
+def test_streamed_equals_sequential(rng):
+    """Acceptance C5 shape (test_acceptance.py:144-163)."""
+    px = rng.integers(0, 256, (256, 256), dtype=np.uint8)
+    img, spec = ih.GrayImage(px), ih.BinSpec.uniform(64)
+    plan = ih.plan_tiles(256, 256, 64, 80_000)
+    assert len(plan.bin_chunks) >= 4 and plan.strips >= 4
+    sink = ih.ArraySink(256, 256, 64)
+    summary = ih.compute_streamed(img, spec, plan, sink)
+    assert np.array_equal(sink.counts, O.compute_crossweave(px, spec.table, 64))
+    assert summary.peak_bytes <= 80_000
+
+
+def test_wavefront_trace_dependency_order(rng):
+    px = rng.integers(0, 256, (50, 70), dtype=np.uint8)
+    trace = []
+    ih.compute_wavefront(ih.GrayImage(px), ih.BinSpec.uniform(4), 16, workers=4, trace=trace)
+    ni, nj = -(-50 // 16), -(-70 // 16)
+    started = [e[1:] for e in trace if e[0] == "start"]
+    assert sorted(started) == sorted((i, j) for i in range(ni) for j in range(nj))
+    done = set()
+    for ev, i, j in trace:
+        if ev == "start":
+            assert i == 0 or (i - 1, j) in done
+            assert j == 0 or (i, j - 1) in done
+        else:
+            done.add((i, j))
+
+
+def test_native_library_is_the_one_loaded():
+    from paper_1711_01919_b200 import _native
+
+    maps = open(f"/proc/{os.getpid()}/maps").read()
+    assert _native.LIB_PATH in maps
