@@ -60,6 +60,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb) {
   p.R = p.cpl == 1 ? 4 : p.cpl == 2 ? 2 : 1;
   const int64_t r_env = env_int("IH_ROWS_PER_BATCH", 0);
   if (r_env == 1 || r_env == 2 || r_env == 4) p.R = (int)r_env;
+  if (p.cpl == 4 && p.R > 2) p.R = 2;  // register budget (128/thread at 16 warps)
   p.ngroups = (nb + ih::kGroup - 1) / ih::kGroup;
   p.nbp = p.ngroups * ih::kGroup;
   // Enough warps in flight to saturate HBM writes; split rows into segments

@@ -55,9 +55,11 @@ __device__ __forceinline__ void st_stream(uint32_t* p, uint32_t a) {
 
 // Build the packed one-hot table of one bin group in shared memory:
 // oh[v] = 1 << 8*(rel(v) - 4g) when rel(v) is in the group, else 0;
-// oh[256] = 0 is the "column beyond the image edge" entry.
+// oh[256..511] = 0 are the "column beyond the image edge" entries, indexed as
+// (pixel | 256) so the edge mask costs one OR.
+constexpr int kOneHotEntries = 512;
 __device__ __forceinline__ void build_onehot(uint32_t* oh, const RelLut& lut, int g) {
-  for (int v = threadIdx.x; v < 257; v += blockDim.x) {
+  for (int v = threadIdx.x; v < kOneHotEntries; v += blockDim.x) {
     uint32_t word = 0;
     if (v < 256) {
       uint32_t d = (uint32_t)lut.rel[v] - (uint32_t)(g * kGroup);
@@ -69,7 +71,7 @@ __device__ __forceinline__ void build_onehot(uint32_t* oh, const RelLut& lut, in
 
 // Load the 4 pixels of one lane in one chunk row and return their 4 one-hot
 // words through the table.  `inval` has bit 8 set for pixel slots at or
-// beyond the right image edge (they map to oh[256] == 0).
+// beyond the right image edge (they map to oh[256 + byte] == 0).
 template <bool ALIGNED>
 __device__ __forceinline__ void load_onehot4(const uint8_t* row, int64_t c, int64_t W,
                                              const uint32_t* oh, const uint32_t inval[4],

@@ -127,7 +127,7 @@ struct ScanArgs {
 
 template <int CPL, int R, bool VEC, bool ALIGNED>
 __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
-  __shared__ uint32_t oh[257];
+  __shared__ uint32_t oh[kOneHotEntries];
   __shared__ uint4 tot[2][R][32];
 
   const int lane = threadIdx.x & 31;
@@ -296,7 +296,7 @@ template <bool VEC, bool ALIGNED>
 __global__ void __launch_bounds__(256) k1_rowscan(const uint8_t* __restrict__ imgs, int64_t H,
                                                    int64_t W, int64_t pitch, int64_t fstride,
                                                    int nb, RelLut lut, uint32_t* __restrict__ out) {
-  __shared__ uint32_t oh[257];
+  __shared__ uint32_t oh[kOneHotEntries];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int g = blockIdx.x;

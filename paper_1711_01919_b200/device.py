@@ -209,7 +209,7 @@ def upload_image(pixels: np.ndarray, device=None) -> torch.Tensor:
     (aligned 32-bit pixel loads in the kernels for every width).  Returns the
     (H, W) view."""
     dev = require_cuda(device)
-    px = np.ascontiguousarray(pixels, dtype=np.uint8)
+    px = np.require(pixels, dtype=np.uint8, requirements=["C", "W"])  # torch needs writable
     H, W = px.shape
     if W % 16 == 0:
         return torch.from_numpy(px).to(dev)

@@ -1,0 +1,47 @@
+"""Tuning sweep of the K2 plan knobs (env vars read per call) on several workloads."""
+import json, os, sys, itertools
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from paper_1711_01919_b200 import device
+
+PEAK = 6555.5
+def synth(w, h, seed):
+    rng = np.random.default_rng(np.random.SeedSequence([seed, w, h]))
+    return rng.integers(0, 256, size=(h, w), dtype=np.uint8)
+
+WL = {
+  "hd64": (1920, 1080, 32, 64, None),
+  "hd1": (1920, 1080, 32, 1, None),
+  "4k128": (3840, 2160, 128, 1, None),
+  "4k128/8": (3840, 2160, 128, 1, (0, 16)),
+  "8k256/8": (8192, 8192, 256, 1, (0, 32)),
+  "512": (512, 512, 32, 1, None),
+}
+def run(name, reps=5, kernel="auto"):
+    W, H, B, F, br = WL[name]
+    frames = torch.from_numpy(np.stack([synth(W, H, k) for k in range(min(F, 8))])).cuda()
+    if F > 8: frames = frames.repeat((F + 7) // 8, 1, 1)[:F].contiguous()
+    lut = ((np.arange(256) * B) // 256).astype(np.uint8)
+    nb = B if br is None else br[1] - br[0]
+    out = device.empty_output(F, nb, H, W, "cuda")
+    for _ in range(3): device.integral_histogram(frames, lut, B, bin_range=br, out=out, kernel=kernel)
+    s, e = torch.cuda.Event(True), torch.cuda.Event(True)
+    torch.cuda.synchronize(); s.record()
+    for _ in range(reps): device.integral_histogram(frames, lut, B, bin_range=br, out=out, kernel=kernel)
+    e.record(); torch.cuda.synchronize()
+    ms = s.elapsed_time(e) / reps
+    alg = F * (H * W + 256 + 4 * nb * H * W)
+    return ms, alg / ms / 1e6
+res = []
+names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(WL)
+for name in names:
+    for kern in ("auto", "crossweave"):
+        if kern == "crossweave":
+            for k in ("IH_ROWS_PER_BATCH", "IH_TARGET_WARPS"): os.environ.pop(k, None)
+            ms, gbs = run(name, kernel=kern)
+            print(json.dumps({"wl": name, "kernel": kern, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)
+            continue
+        for R, tw in itertools.product((1, 2, 4), (148 * 8, 148 * 16, 148 * 24, 148 * 48)):
+            os.environ["IH_ROWS_PER_BATCH"] = str(R); os.environ["IH_TARGET_WARPS"] = str(tw)
+            ms, gbs = run(name)
+            print(json.dumps({"wl": name, "R": R, "tw": tw, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)
