@@ -57,7 +57,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb) {
   else return p;  // cpl = 0: use the cross-weave kernels
   p.nwarps = (int)((nchunks + p.cpl - 1) / p.cpl);
   p.Wp = (int64_t)p.nwarps * p.cpl * ih::kChunk;
-  p.R = p.cpl == 1 ? 4 : p.cpl == 2 ? 2 : 1;
+  p.R = p.cpl == 4 ? 2 : 4;  // tuned on B200 (scripts/sweep.py, profiles/)
   const int64_t r_env = env_int("IH_ROWS_PER_BATCH", 0);
   if (r_env == 1 || r_env == 2 || r_env == 4) p.R = (int)r_env;
   if (p.cpl == 4 && p.R > 2) p.R = 2;  // register budget (128/thread at 16 warps)
@@ -66,7 +66,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb) {
   // Enough warps in flight to saturate HBM writes; split rows into segments
   // only when frames x groups alone do not provide them (each extra segment
   // costs a colcounts/colprefix table of 1/S of the output, mostly in L2).
-  const int64_t target = env_int("IH_TARGET_WARPS", (int64_t)kNumSMs * 24);
+  const int64_t target = env_int("IH_TARGET_WARPS", (int64_t)kNumSMs * 32);
   const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", 48);
   const int64_t base = frames * p.ngroups * p.nwarps;
   int64_t nseg = (target + base - 1) / base;
@@ -143,6 +143,13 @@ bool aligned_rows(const Call& c) {
   return ((uintptr_t)c.img % 4 == 0) && (c.pitch % 4 == 0) && (c.fstride % 4 == 0);
 }
 
+// TMA bulk copies need 16-byte aligned rows; a row copy reads round_up(W, 16)
+// bytes, which stays inside the pitched row because pitch % 16 == 0.
+bool tma_rows(const Call& c) {
+  return ((uintptr_t)c.img % 16 == 0) && (c.pitch % 16 == 0) && (c.fstride % 16 == 0) &&
+         env_int("IH_NO_TMA", 0) == 0;
+}
+
 ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
   if (c.kernel != IH_KERNEL_SINGLE_PASS || c.plan.nseg <= 1) return IH_OK;
   const K2Plan& p = c.plan;
@@ -163,16 +170,28 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
   return IH_OK;
 }
 
+template <int CPL, int R, bool VEC, bool TMA>
+ih_status launch_k2_v(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads) {
+  auto kern = ih::k2_scan<CPL, R, VEC, TMA>;
+  size_t smem = TMA ? (size_t)ih::Ring<R>::kStages * R * a.Wp : 0;
+  if (smem > 48 * 1024) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+        cudaSuccess)
+      return cuda_fail("k2_scan smem attribute");
+  }
+  kern<<<grid, threads, smem, c.stream>>>(a, c.lut);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_scan");
+  return IH_OK;
+}
+
 template <int CPL, int R>
 ih_status launch_k2_cr(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads) {
   const bool vec = (c.W % 4) == 0;
-  const bool al = aligned_rows(c);
-  if (vec && al) ih::k2_scan<CPL, R, true, true><<<grid, threads, 0, c.stream>>>(a, c.lut);
-  else if (vec) ih::k2_scan<CPL, R, true, false><<<grid, threads, 0, c.stream>>>(a, c.lut);
-  else if (al) ih::k2_scan<CPL, R, false, true><<<grid, threads, 0, c.stream>>>(a, c.lut);
-  else ih::k2_scan<CPL, R, false, false><<<grid, threads, 0, c.stream>>>(a, c.lut);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_scan");
-  return IH_OK;
+  const bool tma = tma_rows(c);
+  if (vec && tma) return launch_k2_v<CPL, R, true, true>(c, a, grid, threads);
+  if (vec) return launch_k2_v<CPL, R, true, false>(c, a, grid, threads);
+  if (tma) return launch_k2_v<CPL, R, false, true>(c, a, grid, threads);
+  return launch_k2_v<CPL, R, false, false>(c, a, grid, threads);
 }
 
 ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
@@ -212,6 +231,7 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
   a.S = p.S;
   a.nseg = p.nseg;
   a.Wp = p.Wp;
+  a.row_bytes = (uint32_t)((c.W + 15) / 16 * 16);
   a.colpre = p.nseg > 1 ? (const uint32_t*)ws : nullptr;
   a.out = out;
   dim3 grid((unsigned)p.ngroups, (unsigned)p.nseg, (unsigned)c.frames);

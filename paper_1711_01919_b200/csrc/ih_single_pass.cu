@@ -109,10 +109,12 @@ __global__ void __launch_bounds__(256) k2_colprefix(uint32_t* __restrict__ ws, i
 
 // ---------------------------------------------------------------------------
 // k2_scan: the single pass.  Template parameters:
-//   CPL     chunks per lane (warp covers CPL*128 columns)
-//   R       rows per barrier batch
-//   VEC     W % 4 == 0 (16-byte output stores legal)
-//   ALIGNED image rows 4-byte aligned (one 32-bit pixel load per lane-chunk)
+//   CPL  chunks per lane (warp covers CPL*128 columns)
+//   R    rows per barrier batch
+//   VEC  W % 4 == 0 (16-byte output stores legal)
+//   TMA  image rows 16-byte aligned: rows are staged into a shared-memory ring
+//        by cp.async.bulk (TMA bulk copies, mbarrier completion), NST batches
+//        ahead of the consumers; otherwise lanes load pixels with LDG.
 // ---------------------------------------------------------------------------
 struct ScanArgs {
   const uint8_t* img;
@@ -120,15 +122,68 @@ struct ScanArgs {
   int nb;          // slab bins (bin_hi - bin_lo)
   int nbp;         // padded to a multiple of 4
   int S, nseg;     // segment rows, segments per frame
-  int64_t Wp;      // padded width (multiple of 128)
+  int64_t Wp;      // padded width (multiple of 128) = row stride of the smem ring
+  uint32_t row_bytes;      // bytes copied per row by TMA = round_up(W, 16)
   const uint32_t* colpre;  // ws (nseg > 1) or nullptr
   uint32_t* out;
 };
 
-template <int CPL, int R, bool VEC, bool ALIGNED>
+template <int R>
+struct Ring {
+  static constexpr int kStages = R >= 4 ? 2 : (R == 2 ? 4 : 8);  // 8 rows in flight
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA 1D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0).
+__device__ __forceinline__ void tma_row(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Inclusive warp scan with the lane predicate folded into the shuffle
+// (shfl.sync.up returns p = source lane valid) -> SHFL + predicated IADD.
+__device__ __forceinline__ uint32_t warp_scan_pred(uint32_t x) {
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    asm volatile(
+        "{\n\t.reg .b32 y;\n\t.reg .pred p;\n\t"
+        "shfl.sync.up.b32 y|p, %0, %1, 0, -1;\n\t"
+        "@p add.u32 %0, %0, y;\n\t}"
+        : "+r"(x)
+        : "r"(d));
+  }
+  return x;
+}
+
+template <int CPL, int R, bool VEC, bool TMA>
 __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
+  constexpr int NST = Ring<R>::kStages;
   __shared__ uint32_t oh[kOneHotEntries];
   __shared__ uint4 tot[2][R][32];
+  __shared__ __align__(8) uint64_t full_bar[NST];
+  extern __shared__ __align__(128) uint8_t ring[];  // [NST][R][Wp] image rows (TMA)
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
@@ -136,28 +191,31 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
   const int s = blockIdx.y;
   const int64_t f = blockIdx.z;
   const int64_t H = a.H, W = a.W;
+  const uint8_t* img = a.img + f * a.fstride;
+  const int64_t rs = (int64_t)s * a.S;
+  const int64_t re = (rs + a.S < H ? rs + a.S : H);
+  const int nbatch = (int)((re - rs + R - 1) / R);
 
   build_onehot(oh, lut, g);
+  if (TMA && threadIdx.x == 0) {
+    for (int i = 0; i < NST; ++i) mbar_init(&full_bar[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
 
-  // column of slot j of chunk k for this lane: c0[k] + j
-  int64_t c0[CPL];
+  // lane columns: c0[k] + j, j = 0..3
+  int c0[CPL];
   uint32_t inval[CPL][4];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
-    c0[k] = (int64_t)(warp * CPL + k) * kChunk + lane * 4;
+    c0[k] = (warp * CPL + k) * kChunk + lane * 4;
 #pragma unroll
     for (int j = 0; j < 4; ++j) inval[k][j] = (c0[k] + j < W) ? 0u : 256u;
   }
 
-  // output plane bases of the 4 bins of this group (bins >= nb are masked)
-  uint32_t* plane[kGroup];
-  bool bin_ok[kGroup];
-#pragma unroll
-  for (int i = 0; i < kGroup; ++i) {
-    const int b = g * kGroup + i;
-    bin_ok[i] = b < a.nb;
-    plane[i] = a.out + ((f * a.nb + (bin_ok[i] ? b : 0)) * H) * W;
-  }
+  // output: bin i of this group at plane0 + i * plane_stride (bins >= nb masked)
+  const int64_t plane_elems = H * W;
+  uint32_t* plane0 = a.out + (f * a.nb + (int64_t)g * kGroup) * plane_elems;
+  const int nbins_here = min(kGroup, a.nb - g * kGroup);
 
   uint32_t acc[CPL][4][kGroup];
 #pragma unroll
@@ -167,7 +225,19 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
 #pragma unroll
       for (int i = 0; i < kGroup; ++i) acc[k][j][i] = 0u;
 
-  __syncthreads();  // oh[] ready
+  __syncthreads();  // oh[] and barriers ready
+
+  auto issue = [&](int b) {  // producer: thread 0 only
+    const int stage = b % NST;
+    const int64_t r0 = rs + (int64_t)b * R;
+    const int rows = (int)(re - r0 < R ? re - r0 : R);
+    mbar_expect_tx(&full_bar[stage], (uint32_t)rows * a.row_bytes);
+    for (int rr = 0; rr < rows; ++rr)
+      tma_row(ring + ((size_t)stage * R + rr) * a.Wp, img + (r0 + rr) * a.pitch, a.row_bytes,
+              &full_bar[stage]);
+  };
+  if (TMA && threadIdx.x == 0)
+    for (int b = 0; b < NST && b < nbatch; ++b) issue(b);
 
   // ---- segment carry: acc(c) = sum_{c' <= c} colpre[f][s][b][c'] = H_b(r_s - 1, c)
   if (s > 0) {
@@ -188,7 +258,7 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
       }
 #pragma unroll
       for (int i = 0; i < kGroup; ++i) {
-        const uint32_t x = warp_incl_scan(lt[i], lane);
+        const uint32_t x = warp_scan_pred(lt[i]);
         const uint32_t ex = x - lt[i] + run[i];
 #pragma unroll
         for (int j = 0; j < 4; ++j) acc[k][j][i] += ex;
@@ -209,29 +279,35 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
     __syncthreads();  // tot[0] is reused by the first batch
   }
 
-  const uint8_t* img = a.img + f * a.fstride;
-  const int64_t rs = (int64_t)s * a.S;
-  const int64_t re = (rs + a.S < H ? rs + a.S : H);
+  int64_t row_off = rs * W;  // element offset of the current row within a plane
+  for (int b = 0; b < nbatch; ++b) {
+    const int buf = b & 1;
+    const int64_t r0 = rs + (int64_t)b * R;
+    const int rows = (int)(re - r0 < R ? re - r0 : R);
+    const int stage = b % NST;
+    if (TMA) mbar_wait(&full_bar[stage], (uint32_t)((b / NST) & 1));
 
-  int buf = 0;
-  for (int64_t r0 = rs; r0 < re; r0 += R, buf ^= 1) {
-    uint32_t v[R][CPL][4];   // packed in-chunk inclusive row prefix, 4 bins per word
-    uint32_t ct[R][CPL];     // packed chunk totals
+    uint32_t v[R][CPL][4];  // packed in-chunk inclusive row prefix, 4 bins per word
+    uint32_t ct[R][CPL];    // packed chunk totals
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const int64_t r = r0 + rr;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
-        uint32_t o[4];
-        if (r < re) {
-          load_onehot4<ALIGNED>(img + r * a.pitch, c0[k], W, oh, inval[k], o);
-        } else {
-          o[0] = o[1] = o[2] = o[3] = 0u;
+        uint32_t o[4] = {0u, 0u, 0u, 0u};
+        if (rr < rows) {
+          if (TMA) {
+            const uint32_t px = *reinterpret_cast<const uint32_t*>(
+                ring + ((size_t)stage * R + rr) * a.Wp + c0[k]);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] = oh[((px >> (8 * j)) & 0xffu) | inval[k][j]];
+          } else {
+            load_onehot4<false>(img + (r0 + rr) * a.pitch, c0[k], W, oh, inval[k], o);
+          }
         }
         const uint32_t l1 = o[0] + o[1];
         const uint32_t l2 = l1 + o[2];
         const uint32_t l3 = l2 + o[3];
-        const uint32_t x = warp_incl_scan(l3, lane);
+        const uint32_t x = warp_scan_pred(l3);
         const uint32_t ex = x - l3;
         v[rr][k][0] = o[0] + ex;
         v[rr][k][1] = l1 + ex;
@@ -248,14 +324,14 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
         tot[buf][rr][warp] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
     }
-    __syncthreads();
+    __syncthreads();  // totals visible; every warp is done reading ring stage `stage`
+    if (TMA && threadIdx.x == 0 && b + NST < nbatch) issue(b + NST);
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const int64_t r = r0 + rr;
       const uint4 t = lane < warp ? tot[buf][rr][lane] : make_uint4(0u, 0u, 0u, 0u);
       uint32_t run[kGroup] = {__reduce_add_sync(kFull, t.x), __reduce_add_sync(kFull, t.y),
                               __reduce_add_sync(kFull, t.z), __reduce_add_sync(kFull, t.w)};
-      if (r < re) {
+      if (rr < rows) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
 #pragma unroll
@@ -264,22 +340,25 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
             for (int i = 0; i < kGroup; ++i) acc[k][j][i] += run[i] + byte_of(v[rr][k][j], i);
 #pragma unroll
           for (int i = 0; i < kGroup; ++i) run[i] += byte_of(ct[rr][k], i);
-          const int64_t c = c0[k];
+          const int c = c0[k];
           if (c < W) {
+            uint32_t* p = plane0 + row_off + c;
 #pragma unroll
             for (int i = 0; i < kGroup; ++i) {
-              if (!bin_ok[i]) continue;
-              uint32_t* p = plane[i] + r * W + c;
-              if (VEC) {
-                st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
-              } else {
+              if (i < nbins_here) {
+                if (VEC) {
+                  st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
+                } else {
 #pragma unroll
-                for (int j = 0; j < 4; ++j)
-                  if (c + j < W) st_stream(p + j, acc[k][j][i]);
+                  for (int j = 0; j < 4; ++j)
+                    if (c + j < W) st_stream(p + j, acc[k][j][i]);
+                }
               }
+              p += plane_elems;
             }
           }
         }
+        row_off += W;
       }
     }
   }

@@ -41,7 +41,7 @@ for name in names:
             ms, gbs = run(name, kernel=kern)
             print(json.dumps({"wl": name, "kernel": kern, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)
             continue
-        for R, tw in itertools.product((1, 2, 4), (148 * 8, 148 * 16, 148 * 24, 148 * 48)):
+        for R, tw in itertools.product((1, 2, 4), (148 * 16, 148 * 32, 148 * 64)):
             os.environ["IH_ROWS_PER_BATCH"] = str(R); os.environ["IH_TARGET_WARPS"] = str(tw)
             ms, gbs = run(name)
             print(json.dumps({"wl": name, "R": R, "tw": tw, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)

@@ -25,7 +25,7 @@ def crc_of(t) -> str:
 
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
-    for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS"):
+    for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -99,12 +99,16 @@ SHAPES = [(1, 1), (1, 193), (193, 1), (7, 131), (61, 257), (128, 128), (96, 500)
 
 @pytest.mark.parametrize("nseg", [0, 2, 3, 7])
 @pytest.mark.parametrize("rows_per_batch", [1, 2, 4])
-def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch):
-    """Force K2 row segmentation (colcounts/colprefix/carry-init path) and
-    every barrier batch size; compare with the oracle bit for bit."""
+@pytest.mark.parametrize("tma", [True, False])
+def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch, tma):
+    """Force K2 row segmentation (colcounts/colprefix/carry-init path), every
+    barrier batch size, and both input paths (TMA smem ring / LDG); compare
+    with the oracle bit for bit."""
     if nseg:
         monkeypatch.setenv("IH_NSEG", str(nseg))
     monkeypatch.setenv("IH_ROWS_PER_BATCH", str(rows_per_batch))
+    if not tma:
+        monkeypatch.setenv("IH_NO_TMA", "1")
     for (h, w) in SHAPES:
         bins = int(rng.choice([1, 3, 5, 16, 64]))
         px = rng.integers(0, 256, (h, w), dtype=np.uint8)
