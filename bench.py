@@ -72,7 +72,7 @@ def committed_traffic():
 
 
 class ClockSampler:
-    """SM clocks and throttle reasons sampled through NVML every 100 ms while
+    """SM clocks and throttle reasons sampled through NVML every 5 ms while
     the timed region runs (the recipe's nvidia-smi fields, read directly)."""
 
     REASONS = {  # nvmlClocksEventReason* bits
@@ -102,7 +102,7 @@ class ClockSampler:
             for name, bit in self.REASONS.items():
                 if bits & bit:
                     self.reasons.add(name)
-            self._stop.wait(0.1)
+            self._stop.wait(0.005)
 
     def __enter__(self):
         self.thread = threading.Thread(target=self._safe_run, daemon=True)
@@ -185,9 +185,20 @@ def run_ours(args, rank, world, local_rank):
     import paper_1711_01919_b200 as ih
     from paper_1711_01919_b200 import device, pipeline, sharding
 
-    torch.cuda.set_device(local_rank)
-    dev = torch.device("cuda", local_rank)
+    dev_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
     spec = ih.BinSpec.uniform(BINS)
+
+    def reduce_max(vals):
+        """Max over ranks (NCCL needs CUDA tensors; gloo is used only for the
+        single-GPU path test of this code)."""
+        if world == 1:
+            return list(vals)
+        on = dev if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor(list(vals), dtype=torch.float64, device=on)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
     f0, f1 = sharding.frame_shards(FRAMES, world)[rank]
     nloc = f1 - f0
     host_frames = np.stack([synth_image(WIDTH, HEIGHT, k) for k in range(f0, f1)])
@@ -216,7 +227,7 @@ def run_ours(args, rank, world, local_rank):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    with ClockSampler(local_rank) as clocks:
+    with ClockSampler(dev_index) as clocks:
         barrier()
         for k in range(args.steps):
             starts[k].record(stream)
@@ -248,11 +259,7 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(args.e2e_steps):
             pipe.run(h_in, h_out)
         barrier()
-        e2e_s = time.perf_counter() - t0
-        e2e_s_t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
-        if world > 1:
-            dist.all_reduce(e2e_s_t, op=dist.ReduceOp.MAX)
-        e2e_s = float(e2e_s_t.item())
+        e2e_s = reduce_max([time.perf_counter() - t0])[0]
         e2e = {"value": FRAMES * args.e2e_steps / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(pipe.h2d_bytes) * world,
                "d2h_bytes_per_step": int(pipe.d2h_bytes) * world,
@@ -260,11 +267,8 @@ def run_ours(args, rank, world, local_rank):
         crc_ok = crc_ok and f"{zlib.crc32(h_out[0].numpy().tobytes()):08x}" == gold[f0]
         del h_out, h_in, pipe
 
-    t = torch.tensor([total_ms, scan_ms, prep_ms, 0.0 if crc_ok else 1.0], dtype=torch.float64,
-                     device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total_ms, scan_ms, prep_ms, bad = (float(x) for x in t.tolist())
+    total_ms, scan_ms, prep_ms, bad = reduce_max([total_ms, scan_ms, prep_ms,
+                                                  0.0 if crc_ok else 1.0])
     if rank != 0:
         return
     value = FRAMES * args.steps / (total_ms / 1000.0)
@@ -303,7 +307,7 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -323,8 +327,13 @@ def main():
         import torch
         import torch.distributed as dist
 
-        torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("IH_BENCH_BACKEND", "nccl")  # gloo: 1-GPU path test only
+        dev_index = local_rank % torch.cuda.device_count()
+        torch.cuda.set_device(dev_index)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
+        else:
+            dist.init_process_group(backend)
     try:
         run_ours(args, rank, world, local_rank)
     finally:

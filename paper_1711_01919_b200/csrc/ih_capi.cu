@@ -45,39 +45,123 @@ struct K2Plan {
   int nseg = 1;      // row segments per frame
   int S = 0;         // rows per segment
   int64_t Wp = 0;    // padded width = nwarps * cpl * 128
+  int carry = 0;     // ih::Carry: NONE (nseg == 1), TABLE or LOOKBACK
+  bool big = false;  // 1024-thread instantiation (up to 32 warps, <= 64 registers)
+  bool vec = true;   // W % 4 == 0
+  bool tma = true;   // 16-byte aligned rows
 };
 
-K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb) {
+using K2Fn = void (*)(ih::ScanArgs, ih::RelLut);
+
+template <int CPL, int R, bool VEC, bool TMA, int MAXT>
+K2Fn pick_carry(int carry) {
+  switch (carry) {
+    case ih::CARRY_TABLE: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_TABLE, MAXT>;
+    case ih::CARRY_LOOKBACK: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_LOOKBACK, MAXT>;
+    default: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_NONE, MAXT>;
+  }
+}
+template <int CPL, int R>
+K2Fn pick_vt(const K2Plan& p) {
+  if constexpr (CPL == 1) {  // 1024-thread variants: CPL 1, aligned fast path only
+    if (p.big) return pick_carry<CPL, R, true, true, 1024>(p.carry);
+  } else {
+    if (p.big) return nullptr;
+  }
+  if (p.vec && p.tma) return pick_carry<CPL, R, true, true, 512>(p.carry);
+  if (p.vec) return pick_carry<CPL, R, true, false, 512>(p.carry);
+  if (p.tma) return pick_carry<CPL, R, false, true, 512>(p.carry);
+  return pick_carry<CPL, R, false, false, 512>(p.carry);
+}
+// The instantiated (CPL, R) pairs; plan_k2 only produces these.
+K2Fn pick_k2(const K2Plan& p) {
+  switch (p.cpl * 10 + p.R) {
+    case 11: return pick_vt<1, 1>(p);
+    case 12: return pick_vt<1, 2>(p);
+    case 14: return pick_vt<1, 4>(p);
+    case 21: return pick_vt<2, 1>(p);
+    case 22: return pick_vt<2, 2>(p);
+    case 41: return pick_vt<4, 1>(p);
+    default: return nullptr;
+  }
+}
+size_t k2_ring_smem(const K2Plan& p) {
+  if (!p.tma) return 0;
+  const int nst = p.R >= 4 ? 2 : (p.R == 2 ? 4 : 8);  // ih::Ring<R>::kStages
+  return (size_t)nst * p.R * p.Wp;
+}
+
+// Resident CTAs per SM for the plan's kernel (occupancy API); a register-based
+// estimate when no device is present (ih_workspace_bytes on a CPU host).
+int ctas_per_sm(const K2Plan& p) {
+  K2Fn fn = pick_k2(p);
+  const size_t smem = k2_ring_smem(p);
+  int n = 0;
+  if (fn && (smem <= 48 * 1024 ||
+             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
+                 cudaSuccess) &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, p.nwarps * 32, smem) == cudaSuccess &&
+      n > 0)
+    return n;
+  cudaGetLastError();  // clear a sticky "no device" error
+  const int regs = p.cpl == 1 ? 56 : p.cpl == 2 ? (p.big ? 64 : 96) : 128;
+  n = 65536 / (regs * p.nwarps * 32);
+  return n < 1 ? 1 : n;
+}
+
+K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma) {
   K2Plan p;
+  p.vec = vec;
+  p.tma = tma;
   const int64_t nchunks = (W + ih::kChunk - 1) / ih::kChunk;
-  // at most 16 warps per CTA (<= 128 registers per thread, no spills)
-  if (nchunks <= 16) p.cpl = 1;
-  else if (nchunks <= 32) p.cpl = 2;
-  else if (nchunks <= 64) p.cpl = 4;
-  else return p;  // cpl = 0: use the cross-weave kernels
+  if (vec && tma && env_int("IH_NO_BIG", 0) == 0 && nchunks > 16 && nchunks <= 32) {
+    // W in (2048, 4096]: one 1024-thread CTA per SM, CPL 1 at <= 64 registers
+    p.big = true;
+    p.cpl = 1;
+  } else if (nchunks <= 16) {  // at most 16 warps per CTA (<= 128 registers)
+    p.cpl = 1;
+  } else if (nchunks <= 32) {
+    p.cpl = 2;
+  } else if (nchunks <= 64) {
+    p.cpl = 4;
+  } else {
+    return p;  // cpl = 0: use the cross-weave kernels
+  }
   p.nwarps = (int)((nchunks + p.cpl - 1) / p.cpl);
   p.Wp = (int64_t)p.nwarps * p.cpl * ih::kChunk;
-  p.R = p.cpl == 4 ? 2 : 4;  // tuned on B200 (scripts/sweep.py, profiles/)
+  // rows per barrier batch: tuned on B200 (scripts/sweep*.py, profiles/); the
+  // caps keep the accumulators + batch state inside the register budget
+  p.R = p.cpl == 1 ? 4 : p.cpl == 2 ? 2 : 1;
   const int64_t r_env = env_int("IH_ROWS_PER_BATCH", 0);
   if (r_env == 1 || r_env == 2 || r_env == 4) p.R = (int)r_env;
-  if (p.cpl == 4 && p.R > 2) p.R = 2;  // register budget (128/thread at 16 warps)
+  const int rmax = p.cpl == 1 ? 4 : p.cpl == 2 ? 2 : 1;
+  if (p.R > rmax) p.R = rmax;
   p.ngroups = (nb + ih::kGroup - 1) / ih::kGroup;
   p.nbp = p.ngroups * ih::kGroup;
-  // Enough warps in flight to saturate HBM writes; split rows into segments
-  // only when frames x groups alone do not provide them (each extra segment
-  // costs a colcounts/colprefix table of 1/S of the output, mostly in L2).
-  const int64_t target = env_int("IH_TARGET_WARPS", (int64_t)kNumSMs * 32);
+  p.carry = ih::CARRY_TABLE;  // for the occupancy query; fixed up below
+  // Row segments: enough CTAs for ~4 waves of resident CTAs (measured best for
+  // every frame-batch / single-image class in scripts/sweep*.py); each extra
+  // segment costs a u16 count slot of 1/(2S) of the output, mostly in L2.
+  const double waves = env_int("IH_TARGET_WAVES_X10", 40) / 10.0;
+  const int64_t slots = (int64_t)kNumSMs * ctas_per_sm(p);
   const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", 48);
-  const int64_t base = frames * p.ngroups * p.nwarps;
-  int64_t nseg = (target + base - 1) / base;
+  const int64_t units = frames * p.ngroups;
+  int64_t nseg = (int64_t)(waves * slots / units + 0.999);
   const int64_t max_seg = (H + min_rows - 1) / min_rows;
   if (nseg > max_seg) nseg = max_seg;
   if (nseg > 65535) nseg = 65535;
   if (nseg < 1) nseg = 1;
   const int64_t forced = env_int("IH_NSEG", 0);
   if (forced > 0) nseg = forced < H ? forced : H;
+  // u16 count tables: a segment has < 65536 rows; images taller than 65535
+  // rows cannot use u16 prefixes, so the scan sums count slots (O(nseg^2)):
+  // keep nseg small there
+  if (H > 65535 && nseg > 64) nseg = 64;
   p.S = (int)((H + nseg - 1) / nseg);
+  if (nseg > 1 && p.S > 65535) p.S = 65535;
   p.nseg = (int)((H + p.S - 1) / p.S);
+  if (p.nseg <= 1) p.carry = ih::CARRY_NONE;
+  else p.carry = env_int("IH_CARRY_LOOKBACK", 0) ? ih::CARRY_LOOKBACK : ih::CARRY_TABLE;
   return p;
 }
 
@@ -86,10 +170,29 @@ int resolve_kernel(int kernel, const K2Plan& p) {
   return kernel;
 }
 
-size_t k2_ws_bytes(int64_t frames, const K2Plan& p) {
-  if (p.nseg <= 1) return 0;
-  return (size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint32_t);
+// CARRY_TABLE with few segments skips k2_colprefix: the scan CTA of segment s
+// sums the s count slots above it (fewer bytes than a prefix pass for s <= 8).
+// u16 prefixes need H <= 65535; taller images always sum counts in the scan.
+bool table_prefix_h(const K2Plan& p, int64_t H) {
+  return H <= 65535 && p.nseg > env_int("IH_TABLE_SUM_MAX", 24);
 }
+
+// Workspace layouts.
+//   CARRY_TABLE:    (frames, nseg, nbp, Wp) u32 column-prefix table.
+//   CARRY_LOOKBACK: [ticket | pad 16 B][flags: ntiles u32, 16 B padded]
+//                   [agg: ntiles x 4 x Wp u32][incl: ntiles x 4 x Wp u32]
+int64_t lb_tiles(int64_t frames, const K2Plan& p) { return frames * p.ngroups * p.nseg; }
+size_t lb_header_bytes(int64_t frames, const K2Plan& p) {
+  return 16 + (size_t)((lb_tiles(frames, p) * 4 + 15) / 16 * 16);
+}
+size_t k2_ws_bytes_plan(int64_t frames, const K2Plan& p) {
+  if (p.carry == ih::CARRY_TABLE) return (size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint16_t);
+  if (p.carry == ih::CARRY_LOOKBACK)
+    return lb_header_bytes(frames, p) +
+           2 * (size_t)lb_tiles(frames, p) * ih::kGroup * p.Wp * sizeof(uint32_t);
+  return 0;
+}
+size_t k2_ws_bytes(int64_t frames, const K2Plan& p) { return k2_ws_bytes_plan(frames, p); }
 
 struct Call {
   const uint8_t* img;
@@ -132,7 +235,11 @@ ih_status validate(const uint8_t* img, int64_t frames, int64_t H, int64_t W, int
     const int rel = (int)lut256[v] - bin_lo;
     c->lut.rel[v] = (rel >= 0 && rel < c->nb) ? (uint8_t)rel : (uint8_t)0xff;
   }
-  c->plan = plan_k2(frames, H, W, c->nb);
+  // TMA bulk copies need 16-byte aligned rows; a row copy reads round_up(W, 16)
+  // bytes, which stays inside the pitched row because pitch % 16 == 0.
+  const bool tma = (uintptr_t)img % 16 == 0 && pitch % 16 == 0 && c->fstride % 16 == 0 &&
+                   env_int("IH_NO_TMA", 0) == 0;
+  c->plan = plan_k2(frames, H, W, c->nb, W % 4 == 0, tma);
   c->kernel = resolve_kernel(kernel, c->plan);
   if (c->kernel == IH_KERNEL_SINGLE_PASS && c->plan.cpl == 0)
     return fail(IH_ERR_PARAM, "single-pass kernel supports width <= 8192; use crossweave");
@@ -143,55 +250,48 @@ bool aligned_rows(const Call& c) {
   return ((uintptr_t)c.img % 4 == 0) && (c.pitch % 4 == 0) && (c.fstride % 4 == 0);
 }
 
-// TMA bulk copies need 16-byte aligned rows; a row copy reads round_up(W, 16)
-// bytes, which stays inside the pitched row because pitch % 16 == 0.
-bool tma_rows(const Call& c) {
-  return ((uintptr_t)c.img % 16 == 0) && (c.pitch % 16 == 0) && (c.fstride % 16 == 0) &&
-         env_int("IH_NO_TMA", 0) == 0;
-}
 
 ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
-  if (c.kernel != IH_KERNEL_SINGLE_PASS || c.plan.nseg <= 1) return IH_OK;
+  if (c.kernel != IH_KERNEL_SINGLE_PASS || c.plan.carry == ih::CARRY_NONE) return IH_OK;
   const K2Plan& p = c.plan;
   if (ws_bytes < k2_ws_bytes(c.frames, p) || !ws)
     return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
-  const int nslab64 = (p.nbp + 63) / 64;
-  dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1),
-            (unsigned)(c.frames * nslab64));
-  ih::k2_colcounts<<<grid, 128, 0, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S,
-                                                p.nseg, p.nbp, p.Wp, nslab64, (uint32_t*)ws);
+  if (p.carry == ih::CARRY_LOOKBACK) {  // reset the ticket and the tile flags
+    if (cudaMemsetAsync(ws, 0, lb_header_bytes(c.frames, p), c.stream) != cudaSuccess)
+      return cuda_fail("look-back flag reset");
+    return IH_OK;
+  }
+  const int nslab = (p.nbp + ih::kCountSlab - 1) / ih::kCountSlab;
+  dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)(c.frames * nslab));
+  const bool al = aligned_rows(c);
+  auto kern = al ? ih::k2_colcounts<true> : ih::k2_colcounts<false>;
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)ih::kCountSmem) != cudaSuccess)
+    return cuda_fail("k2_colcounts smem attribute");
+  kern<<<grid, ih::kCountWarps * 32, ih::kCountSmem, c.stream>>>(
+      c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S, p.nseg, p.nbp, p.Wp, nslab, (uint16_t*)ws);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts");
-  const int64_t total = c.frames * p.nbp * p.Wp;
+  if (!table_prefix_h(p, c.H)) return IH_OK;  // the scan kernel sums the count slots
+  const int64_t total = c.frames * p.nbp * p.Wp / 4;
   int64_t blocks = (total + 255) / 256;
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
-  ih::k2_colprefix<<<(unsigned)blocks, 256, 0, c.stream>>>((uint32_t*)ws, c.frames, p.nseg, p.nbp,
+  ih::k2_colprefix<<<(unsigned)blocks, 256, 0, c.stream>>>((uint16_t*)ws, c.frames, p.nseg, p.nbp,
                                                            p.Wp);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colprefix");
   return IH_OK;
 }
 
-template <int CPL, int R, bool VEC, bool TMA>
-ih_status launch_k2_v(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads) {
-  auto kern = ih::k2_scan<CPL, R, VEC, TMA>;
-  size_t smem = TMA ? (size_t)ih::Ring<R>::kStages * R * a.Wp : 0;
-  if (smem > 48 * 1024) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-        cudaSuccess)
-      return cuda_fail("k2_scan smem attribute");
-  }
-  kern<<<grid, threads, smem, c.stream>>>(a, c.lut);
+ih_status launch_k2(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads) {
+  K2Fn fn = pick_k2(c.plan);
+  if (!fn) return fail(IH_ERR_PARAM, "internal: no K2 instantiation for plan");
+  const size_t smem = k2_ring_smem(c.plan);
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
+    return cuda_fail("k2_scan smem attribute");
+  fn<<<grid, threads, smem, c.stream>>>(a, c.lut);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_scan");
   return IH_OK;
-}
-
-template <int CPL, int R>
-ih_status launch_k2_cr(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads) {
-  const bool vec = (c.W % 4) == 0;
-  const bool tma = tma_rows(c);
-  if (vec && tma) return launch_k2_v<CPL, R, true, true>(c, a, grid, threads);
-  if (vec) return launch_k2_v<CPL, R, true, false>(c, a, grid, threads);
-  if (tma) return launch_k2_v<CPL, R, false, true>(c, a, grid, threads);
-  return launch_k2_v<CPL, R, false, false>(c, a, grid, threads);
 }
 
 ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
@@ -218,7 +318,7 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
     return IH_OK;
   }
   const K2Plan& p = c.plan;
-  if (p.nseg > 1 && (ws_bytes < k2_ws_bytes(c.frames, p) || !ws))
+  if (p.carry != ih::CARRY_NONE && (ws_bytes < k2_ws_bytes(c.frames, p) || !ws))
     return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
   ih::ScanArgs a;
   a.img = c.img;
@@ -232,21 +332,20 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
   a.nseg = p.nseg;
   a.Wp = p.Wp;
   a.row_bytes = (uint32_t)((c.W + 15) / 16 * 16);
-  a.colpre = p.nseg > 1 ? (const uint32_t*)ws : nullptr;
+  a.colpre = p.carry == ih::CARRY_TABLE ? (const uint16_t*)ws : nullptr;
+  a.table_is_prefix = table_prefix_h(p, c.H) ? 1 : 0;
+  a.lb_ticket = a.lb_flags = a.lb_agg = a.lb_incl = nullptr;
+  if (p.carry == ih::CARRY_LOOKBACK) {
+    uint8_t* base = (uint8_t*)ws;
+    a.lb_ticket = (uint32_t*)base;
+    a.lb_flags = (uint32_t*)(base + 16);
+    a.lb_agg = (uint32_t*)(base + lb_header_bytes(c.frames, p));
+    a.lb_incl = a.lb_agg + lb_tiles(c.frames, p) * ih::kGroup * p.Wp;
+  }
   a.out = out;
   dim3 grid((unsigned)p.ngroups, (unsigned)p.nseg, (unsigned)c.frames);
   const int threads = p.nwarps * 32;
-  switch (p.cpl * 10 + p.R) {
-    case 14: return launch_k2_cr<1, 4>(c, a, grid, threads);
-    case 12: return launch_k2_cr<1, 2>(c, a, grid, threads);
-    case 24: return launch_k2_cr<2, 4>(c, a, grid, threads);
-    case 22: return launch_k2_cr<2, 2>(c, a, grid, threads);
-    case 11: return launch_k2_cr<1, 1>(c, a, grid, threads);
-    case 21: return launch_k2_cr<2, 1>(c, a, grid, threads);
-    case 42: return launch_k2_cr<4, 2>(c, a, grid, threads);
-    case 41: return launch_k2_cr<4, 1>(c, a, grid, threads);
-    default: return fail(IH_ERR_PARAM, "internal: no K2 instantiation for plan");
-  }
+  return launch_k2(c, a, grid, threads);
 }
 
 }  // namespace
@@ -256,9 +355,17 @@ extern "C" {
 size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
                           int32_t kernel) {
   if (frames < 1 || height < 1 || width < 1 || slab_bins < 1) return 0;
-  K2Plan p = plan_k2(frames, height, width, slab_bins);
-  if (resolve_kernel(kernel, p) != IH_KERNEL_SINGLE_PASS || p.cpl == 0) return 0;
-  return k2_ws_bytes(frames, p);
+  // the plan depends on the input alignment (1024-thread variants need the TMA
+  // path); size the workspace for either
+  size_t n = 0;
+  for (int variant = 0; variant < 4; ++variant) {
+    K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0 && (variant & 1),
+                       (variant & 2) != 0);
+    if (resolve_kernel(kernel, p) != IH_KERNEL_SINGLE_PASS || p.cpl == 0) continue;
+    const size_t b = k2_ws_bytes(frames, p);
+    if (b > n) n = b;
+  }
+  return n;
 }
 
 ih_status ih_ih_prepare(const uint8_t* img, int64_t frames, int64_t height, int64_t width,

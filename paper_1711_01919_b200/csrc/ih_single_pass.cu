@@ -27,83 +27,133 @@
 namespace ih {
 
 // ---------------------------------------------------------------------------
-// k2_colcounts: ws[f][s][b][c] = #{ r in segment s : Q(I(r,c)) = b }, for the
-// 64-bin slab `blockIdx.z % nslab64` of the padded bin range, s < nseg-1.
-// CTA = 128 threads = one 128-column chunk; thread t owns column t (no atomics:
-// hist[b][t] is private to t, bank = t mod 32, conflict-free).
+// k2_colcounts: ws[f][s][b][c] = #{ r in segment s : Q(I(r,c)) = b } (u16) for the
+// 32-bin slab `blockIdx.z % nslab` of the padded bin range, segments s < nseg-1.
+// CTA = 8 warps on the same 128-column chunk, each warp counting a contiguous
+// eighth of the segment's rows (lane = 4 columns, one 32-bit pixel load per
+// row, 8 rows of loads in flight).  Every warp owns a private 16-bit
+// histogram [bin][k][lane] in shared memory (bank = lane: conflict-free, no
+// atomics); the 8 histograms are summed once at the end.  Segment rows are
+// < 65536 (host-enforced).  Pixels past the right edge map to LUT entry 256+.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(128) k2_colcounts(const uint8_t* __restrict__ img,
-                                                     int64_t H, int64_t W, int64_t pitch,
-                                                     int64_t fstride, RelLut lut, int S,
-                                                     int nseg, int nbp, int64_t Wp,
-                                                     int nslab64, uint32_t* __restrict__ ws) {
-  __shared__ uint32_t hist[64][kChunk];
-  __shared__ uint8_t slut[256];
-  const int t = threadIdx.x;
-  const int64_t c = (int64_t)blockIdx.x * kChunk + t;
+constexpr int kCountSlab = 32;
+constexpr int kCountWarps = 8;
+constexpr size_t kCountSmem = (size_t)kCountWarps * kCountSlab * 4 * 32 * sizeof(uint16_t);
+
+template <bool ALIGNED>
+__global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
+    const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
+    RelLut lut, int S, int nseg, int nbp, int64_t Wp, int nslab, uint16_t* __restrict__ ws) {
+  extern __shared__ __align__(16) uint16_t chist[];  // [warp][bin][k][lane]
+  __shared__ uint8_t slut[512];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * kChunk + 4 * lane;
   const int s = blockIdx.y;
-  const int slab = blockIdx.z % nslab64;
-  const int64_t f = blockIdx.z / nslab64;
-  for (int v = t; v < 256; v += 128) slut[v] = lut.rel[v];
-#pragma unroll 8
-  for (int b = 0; b < 64; ++b) hist[b][t] = 0;
+  const int slab = blockIdx.z % nslab;
+  const int64_t f = blockIdx.z / nslab;
+  const uint32_t lo = (uint32_t)slab * kCountSlab;
+  for (int v = threadIdx.x; v < 512; v += blockDim.x) {
+    const uint32_t d = v < 256 ? (uint32_t)lut.rel[v] - lo : 0xffu;
+    slut[v] = d < (uint32_t)kCountSlab ? (uint8_t)d : (uint8_t)0xff;
+  }
+  {
+    uint4* z = reinterpret_cast<uint4*>(chist);
+    for (int i = threadIdx.x; i < (int)(kCountSmem / 16); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  uint32_t inval[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) inval[k] = (c + k < W) ? 0u : 256u;
   __syncthreads();
+  uint16_t* hist = chist + (size_t)warp * kCountSlab * 4 * 32 + lane;  // [bin][k] stride 32
   const uint8_t* base = img + f * fstride;
-  const int64_t r0 = (int64_t)s * S;
-  const int64_t r1 = (r0 + S < H ? r0 + S : H);
-  const uint32_t lo = (uint32_t)slab * 64u;
+  const int64_t seg0 = (int64_t)s * S;
+  const int64_t seg1 = (seg0 + S < H ? seg0 + S : H);
+  const int64_t per = (seg1 - seg0 + kCountWarps - 1) / kCountWarps;
+  const int64_t r0 = seg0 + warp * per;
+  const int64_t r1 = (r0 + per < seg1 ? r0 + per : seg1);
+  auto load_px = [&](int64_t r) -> uint32_t {
+    const uint8_t* row = base + r * pitch + c;
+    if (ALIGNED) return __ldg(reinterpret_cast<const uint32_t*>(row));
+    uint32_t px = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (c + k < W) px |= (uint32_t)__ldg(row + k) << (8 * k);
+    return px;
+  };
+  auto count4 = [&](uint32_t px) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t d = slut[((px >> (8 * k)) & 0xffu) | inval[k]];
+      if (d != 0xffu) hist[(d * 4 + k) * 32] += 1;
+    }
+  };
   if (c < W) {
     int64_t r = r0;
     for (; r + 8 <= r1; r += 8) {
-      uint8_t p[8];
+      uint32_t px[8];
 #pragma unroll
-      for (int k = 0; k < 8; ++k) p[k] = __ldg(base + (r + k) * pitch + c);
+      for (int i = 0; i < 8; ++i) px[i] = load_px(r + i);
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        uint32_t d = (uint32_t)slut[p[k]] - lo;
-        if (d < 64u) hist[d][t] += 1u;
-      }
+      for (int i = 0; i < 8; ++i) count4(px[i]);
     }
-    for (; r < r1; ++r) {
-      uint32_t d = (uint32_t)slut[__ldg(base + r * pitch + c)] - lo;
-      if (d < 64u) hist[d][t] += 1u;
-    }
+    for (; r < r1; ++r) count4(load_px(r));
   }
-  // (no barrier needed: every thread reads back only its own column)
-  const int nbs = min(64, nbp - slab * 64);
-  uint32_t* dst = ws + ((f * nseg + s) * (int64_t)nbp + lo) * Wp + c;
-  for (int b = 0; b < nbs; ++b) dst[(int64_t)b * Wp] = hist[b][t];
+  __syncthreads();
+  // sum the 8 private histograms; item = (bin, lane) -> 4 columns, one 8-byte store
+  const int nbs = min(kCountSlab, nbp - (int)lo);
+  uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp + lo) * Wp + (int64_t)blockIdx.x * kChunk;
+  for (int e = threadIdx.x; e < nbs * 32; e += blockDim.x) {
+    const int l = e & 31, b = e >> 5;
+    uint32_t sum[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+    for (int w = 0; w < kCountWarps; ++w)
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        sum[k] += chist[(size_t)w * kCountSlab * 4 * 32 + (b * 4 + k) * 32 + l];
+    *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) =
+        make_uint2(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16));
+  }
 }
 
 // ---------------------------------------------------------------------------
 // k2_colprefix: in place, ws[f][s][b][c] <- sum_{s' < s} counts[f][s'][b][c]
-// (exclusive prefix over segments; slot nseg-1 is never read as a count).
-// Thread per (f, b, c); loads of the nseg-1 slots are independent.
+// (u16; only used when H <= 65535 so every prefix fits).  Thread per
+// (f, b, 4 columns); loads are issued 8 segments at a time before any store.
+// Slot nseg-1 holds no count on entry.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k2_colprefix(uint32_t* __restrict__ ws, int64_t frames,
+__device__ __forceinline__ uint2 add_u16x4(uint2 a, uint2 b) {  // lanes never carry (< 65536)
+  return make_uint2(a.x + b.x, a.y + b.y);
+}
+
+__global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, int64_t frames,
                                                      int nseg, int nbp, int64_t Wp) {
-  const int64_t plane = (int64_t)nbp * Wp;
-  const int64_t total = frames * plane;
+  const int64_t plane = (int64_t)nbp * Wp;  // elements per segment slot
+  const int64_t quads = plane / 4;
+  const int64_t total = frames * quads;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
        i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = i / plane, rem = i % plane;
-    uint32_t* p = ws + f * nseg * plane + rem;
-    uint32_t run = 0;
+    const int64_t f = i / quads, q = i % quads;
+    uint2* p = reinterpret_cast<uint2*>(ws + f * nseg * plane) + q;
+    const int64_t step = quads;
+    uint2 run = make_uint2(0u, 0u);
     int s = 0;
-    for (; s + 4 <= nseg - 1; s += 4) {
-      uint32_t v0 = p[(s + 0) * plane], v1 = p[(s + 1) * plane];
-      uint32_t v2 = p[(s + 2) * plane], v3 = p[(s + 3) * plane];
-      p[(s + 0) * plane] = run; run += v0;
-      p[(s + 1) * plane] = run; run += v1;
-      p[(s + 2) * plane] = run; run += v2;
-      p[(s + 3) * plane] = run; run += v3;
+    for (; s + 8 <= nseg - 1; s += 8) {
+      uint2 v[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) v[k] = p[(s + k) * step];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        p[(s + k) * step] = run;
+        run = add_u16x4(run, v[k]);
+      }
     }
     for (; s < nseg - 1; ++s) {
-      uint32_t v = p[s * plane];
-      p[s * plane] = run;
-      run += v;
+      const uint2 v = p[s * step];
+      p[s * step] = run;
+      run = add_u16x4(run, v);
     }
-    p[(int64_t)(nseg - 1) * plane] = run;
+    p[(int64_t)(nseg - 1) * step] = run;
   }
 }
 
@@ -124,9 +174,27 @@ struct ScanArgs {
   int S, nseg;     // segment rows, segments per frame
   int64_t Wp;      // padded width (multiple of 128) = row stride of the smem ring
   uint32_t row_bytes;      // bytes copied per row by TMA = round_up(W, 16)
-  const uint32_t* colpre;  // ws (nseg > 1) or nullptr
+  const uint16_t* colpre;  // CARRY_TABLE: (frames, nseg, nbp, Wp) u16 column counts or prefixes
+  int table_is_prefix;     // 1: slot s holds sum_{s'<s} counts (k2_colprefix ran); 0: raw counts
+  uint32_t* lb_ticket;     // CARRY_LOOKBACK: tile ticket counter (zeroed per launch)
+  uint32_t* lb_flags;      //   per-tile status: 0, kFlagAgg, kFlagIncl (zeroed per launch)
+  uint32_t* lb_agg;        //   per-tile column counts      (ntiles, 4, Wp) u32
+  uint32_t* lb_incl;       //   per-tile inclusive prefixes (ntiles, 4, Wp) u32
   uint32_t* out;
 };
+
+// Row-segment carry schemes of k2_scan.
+enum Carry { CARRY_NONE = 0, CARRY_TABLE = 1, CARRY_LOOKBACK = 2 };
+constexpr uint32_t kFlagAgg = 1u, kFlagIncl = 2u;
+
+__device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 template <int R>
 struct Ring {
@@ -177,24 +245,46 @@ __device__ __forceinline__ uint32_t warp_scan_pred(uint32_t x) {
   return x;
 }
 
-template <int CPL, int R, bool VEC, bool TMA>
-__global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
+// MAXT: launch bound -- 512 (<= 16 warps, up to 128 registers) or 1024
+// (<= 32 warps at <= 64 registers: full SM occupancy from one CTA).
+template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT>
+__global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
   constexpr int NST = Ring<R>::kStages;
   __shared__ uint32_t oh[kOneHotEntries];
   __shared__ uint4 tot[2][R][32];
   __shared__ __align__(8) uint64_t full_bar[NST];
+  __shared__ uint32_t s_tile, s_flag;
   extern __shared__ __align__(128) uint8_t ring[];  // [NST][R][Wp] image rows (TMA)
 
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int g = blockIdx.x;
-  const int s = blockIdx.y;
-  const int64_t f = blockIdx.z;
   const int64_t H = a.H, W = a.W;
+
+  // Tile (frame f, bin group g, segment s).  With look-back carries the tile
+  // comes from an atomic ticket, so every tile a CTA waits on has already
+  // started (forward progress); segments of one (f, g) chain are adjacent.
+  int g, s;
+  int64_t f;
+  if (CARRY == CARRY_LOOKBACK) {
+    if (threadIdx.x == 0) s_tile = atomicAdd(a.lb_ticket, 1u);
+    __syncthreads();
+    const uint32_t t = s_tile;
+    s = (int)(t % (uint32_t)a.nseg);
+    g = (int)((t / (uint32_t)a.nseg) % (uint32_t)gridDim.x);
+    f = (int64_t)(t / ((uint32_t)a.nseg * gridDim.x));
+  } else {
+    g = blockIdx.x;
+    s = blockIdx.y;
+    f = blockIdx.z;
+  }
   const uint8_t* img = a.img + f * a.fstride;
   const int64_t rs = (int64_t)s * a.S;
   const int64_t re = (rs + a.S < H ? rs + a.S : H);
   const int nbatch = (int)((re - rs + R - 1) / R);
+  // look-back: segments other than the last count their rows first (pass 0)
+  const bool count_pass = CARRY == CARRY_LOOKBACK && s + 1 < a.nseg;
+  const int nb_count = count_pass ? nbatch : 0;
+  const int nb_total = nb_count + nbatch;
 
   build_onehot(oh, lut, g);
   if (TMA && threadIdx.x == 0) {
@@ -227,9 +317,11 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
 
   __syncthreads();  // oh[] and barriers ready
 
+  // ring batch b -> first row (pass 0 = counting, pass 1 = scan)
+  auto batch_row0 = [&](int b) { return rs + (int64_t)(b < nb_count ? b : b - nb_count) * R; };
   auto issue = [&](int b) {  // producer: thread 0 only
     const int stage = b % NST;
-    const int64_t r0 = rs + (int64_t)b * R;
+    const int64_t r0 = batch_row0(b);
     const int rows = (int)(re - r0 < R ? re - r0 : R);
     mbar_expect_tx(&full_bar[stage], (uint32_t)rows * a.row_bytes);
     for (int rr = 0; rr < rows; ++rr)
@@ -237,23 +329,155 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
               &full_bar[stage]);
   };
   if (TMA && threadIdx.x == 0)
-    for (int b = 0; b < NST && b < nbatch; ++b) issue(b);
+    for (int b = 0; b < NST && b < nb_total; ++b) issue(b);
 
-  // ---- segment carry: acc(c) = sum_{c' <= c} colpre[f][s][b][c'] = H_b(r_s - 1, c)
-  if (s > 0) {
+  // 4 one-hot words of lane columns c0[k]..+3 for row rr of ring batch b
+  auto onehot4 = [&](int b, int rr, int k, uint32_t o[4]) {
+    if (TMA) {
+      const int stage = b % NST;
+      const uint32_t px = *reinterpret_cast<const uint32_t*>(
+          ring + ((size_t)stage * R + rr) * a.Wp + c0[k]);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[j] = oh[((px >> (8 * j)) & 0xffu) | inval[k][j]];
+    } else {
+      load_onehot4<false>(img + (batch_row0(b) + rr) * a.pitch, c0[k], W, oh, inval[k], o);
+    }
+  };
+
+  if (CARRY == CARRY_LOOKBACK) {
+    const int64_t ntile_vec = (int64_t)kGroup * a.Wp;  // u32 per published vector
+    const uint32_t tile = s_tile;
+    uint32_t* flags = a.lb_flags;
+    uint32_t* agg = a.lb_agg;
+    uint32_t* incl = a.lb_incl;
+    // ---- pass 0: per-column counts of this segment's rows for the 4 bins,
+    // 16-bit lanes (bins 0/2 in ce, 1/3 in co); segments are < 65536 rows.
+    if (count_pass) {
+      uint32_t ce[CPL][4], co[CPL][4];
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ce[k][j] = co[k][j] = 0u;
+      for (int b = 0; b < nb_count; ++b) {
+        const int rows = (int)(re - batch_row0(b) < R ? re - batch_row0(b) : R);
+        if (TMA) mbar_wait(&full_bar[b % NST], (uint32_t)((b / NST) & 1));
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          if (rr < rows) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              uint32_t o[4];
+              onehot4(b, rr, k, o);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                ce[k][j] += o[j] & 0x00ff00ffu;
+                co[k][j] += (o[j] >> 8) & 0x00ff00ffu;
+              }
+            }
+          }
+        }
+        __syncthreads();  // ring stage consumed
+        if (TMA && threadIdx.x == 0 && b + NST < nb_total) issue(b + NST);
+      }
+      // publish the aggregate: agg[tile][i][c]
+      uint32_t* dst = agg + (int64_t)tile * ntile_vec;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k) {
+        uint32_t cnt[kGroup][4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          cnt[0][j] = ce[k][j] & 0xffffu;
+          cnt[1][j] = co[k][j] & 0xffffu;
+          cnt[2][j] = ce[k][j] >> 16;
+          cnt[3][j] = co[k][j] >> 16;
+        }
+#pragma unroll
+        for (int i = 0; i < kGroup; ++i)
+          __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + c0[k]),
+                 make_uint4(cnt[i][0], cnt[i][1], cnt[i][2], cnt[i][3]));
+        if (s == 0) {  // segment 0: its aggregate is its inclusive prefix
+#pragma unroll
+          for (int i = 0; i < kGroup; ++i)
+            __stcg(reinterpret_cast<uint4*>(incl + (int64_t)tile * ntile_vec + i * a.Wp + c0[k]),
+                   make_uint4(cnt[i][0], cnt[i][1], cnt[i][2], cnt[i][3]));
+        }
+      }
+      __threadfence();
+      __syncthreads();
+      if (threadIdx.x == 0) st_release_gpu(flags + tile, s == 0 ? kFlagIncl : kFlagAgg);
+    }
+    // ---- look-back: acc = sum over segments s' < s of their column counts
+    if (s > 0) {
+      for (int sp = s - 1; sp >= 0; --sp) {
+        const uint32_t pt = tile - (uint32_t)(s - sp);
+        if (threadIdx.x == 0) {
+          uint32_t v;
+          while ((v = ld_acquire_gpu(flags + pt)) == 0u) __nanosleep(64);
+          s_flag = v;
+        }
+        __syncthreads();
+        const uint32_t v = s_flag;
+        const uint32_t* src = (v == kFlagIncl ? incl : agg) + (int64_t)pt * ntile_vec;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+#pragma unroll
+          for (int i = 0; i < kGroup; ++i) {
+            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(src + i * a.Wp + c0[k]));
+            acc[k][0][i] += x.x;
+            acc[k][1][i] += x.y;
+            acc[k][2][i] += x.z;
+            acc[k][3][i] += x.w;
+          }
+        __syncthreads();  // s_flag reuse
+        if (v == kFlagIncl) break;
+      }
+      if (count_pass) {  // inclusive = exclusive + own aggregate
+        const uint32_t* own = agg + (int64_t)tile * ntile_vec;
+        uint32_t* dst = incl + (int64_t)tile * ntile_vec;
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+#pragma unroll
+          for (int i = 0; i < kGroup; ++i) {
+            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(own + i * a.Wp + c0[k]));
+            __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + c0[k]),
+                   make_uint4(acc[k][0][i] + x.x, acc[k][1][i] + x.y, acc[k][2][i] + x.z,
+                              acc[k][3][i] + x.w));
+          }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_gpu(flags + tile, kFlagIncl);
+      }
+    }
+  } else if (CARRY == CARRY_TABLE && s > 0) {
     const int64_t plane_sz = (int64_t)a.nbp * a.Wp;
-    const uint32_t* cp = a.colpre + (f * a.nseg + s) * plane_sz + (int64_t)g * kGroup * a.Wp;
+    const uint16_t* cp = a.colpre + (f * a.nseg) * plane_sz + (int64_t)g * kGroup * a.Wp;
+    // prefix table: one slot; raw counts: sum slots 0..s-1 here (L2-resident)
+    for (int sp = a.table_is_prefix ? s : 0; sp < (a.table_is_prefix ? s + 1 : s); ++sp) {
+      const uint16_t* q = cp + sp * plane_sz;
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+#pragma unroll
+        for (int i = 0; i < kGroup; ++i) {
+          const uint2 v = *reinterpret_cast<const uint2*>(q + i * a.Wp + c0[k]);
+          acc[k][0][i] += v.x & 0xffffu;
+          acc[k][1][i] += v.x >> 16;
+          acc[k][2][i] += v.y & 0xffffu;
+          acc[k][3][i] += v.y >> 16;
+        }
+    }
+  }
+
+  // ---- segment carry: acc(c) <- sum_{c' <= c} acc(c') = H_b(r_s - 1, c)
+  if (CARRY != CARRY_NONE && s > 0) {
     uint32_t run[kGroup] = {0u, 0u, 0u, 0u};
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
       uint32_t lt[kGroup];
 #pragma unroll
       for (int i = 0; i < kGroup; ++i) {
-        const uint4 v = *reinterpret_cast<const uint4*>(cp + i * a.Wp + c0[k]);
-        acc[k][0][i] = v.x;
-        acc[k][1][i] = v.x + v.y;
-        acc[k][2][i] = v.x + v.y + v.z;
-        acc[k][3][i] = v.x + v.y + v.z + v.w;
+        acc[k][1][i] += acc[k][0][i];
+        acc[k][2][i] += acc[k][1][i];
+        acc[k][3][i] += acc[k][2][i];
         lt[i] = acc[k][3][i];
       }
 #pragma unroll
@@ -279,13 +503,14 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
     __syncthreads();  // tot[0] is reused by the first batch
   }
 
+  // ---- pass 1: the scan
   int64_t row_off = rs * W;  // element offset of the current row within a plane
-  for (int b = 0; b < nbatch; ++b) {
-    const int buf = b & 1;
-    const int64_t r0 = rs + (int64_t)b * R;
+  for (int b = nb_count; b < nb_total; ++b) {
+    const int bi = b - nb_count;
+    const int buf = bi & 1;
+    const int64_t r0 = rs + (int64_t)bi * R;
     const int rows = (int)(re - r0 < R ? re - r0 : R);
-    const int stage = b % NST;
-    if (TMA) mbar_wait(&full_bar[stage], (uint32_t)((b / NST) & 1));
+    if (TMA) mbar_wait(&full_bar[b % NST], (uint32_t)((b / NST) & 1));
 
     uint32_t v[R][CPL][4];  // packed in-chunk inclusive row prefix, 4 bins per word
     uint32_t ct[R][CPL];    // packed chunk totals
@@ -294,16 +519,7 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         uint32_t o[4] = {0u, 0u, 0u, 0u};
-        if (rr < rows) {
-          if (TMA) {
-            const uint32_t px = *reinterpret_cast<const uint32_t*>(
-                ring + ((size_t)stage * R + rr) * a.Wp + c0[k]);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) o[j] = oh[((px >> (8 * j)) & 0xffu) | inval[k][j]];
-          } else {
-            load_onehot4<false>(img + (r0 + rr) * a.pitch, c0[k], W, oh, inval[k], o);
-          }
-        }
+        if (rr < rows) onehot4(b, rr, k, o);
         const uint32_t l1 = o[0] + o[1];
         const uint32_t l2 = l1 + o[2];
         const uint32_t l3 = l2 + o[3];
@@ -324,8 +540,8 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
         tot[buf][rr][warp] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
     }
-    __syncthreads();  // totals visible; every warp is done reading ring stage `stage`
-    if (TMA && threadIdx.x == 0 && b + NST < nbatch) issue(b + NST);
+    __syncthreads();  // totals visible; every warp is done reading the ring stage
+    if (TMA && threadIdx.x == 0 && b + NST < nb_total) issue(b + NST);
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
       const uint4 t = lane < warp ? tot[buf][rr][lane] : make_uint4(0u, 0u, 0u, 0u);
@@ -363,6 +579,7 @@ __global__ void __launch_bounds__(512) k2_scan(ScanArgs a, RelLut lut) {
     }
   }
 }
+
 
 // ---------------------------------------------------------------------------
 // K1 / K1b: the cross-weave (CW-B) analog, strategies.py:118-150.

@@ -16,6 +16,12 @@ WL = {
   "4k128/8": (3840, 2160, 128, 1, (0, 16)),
   "8k256/8": (8192, 8192, 256, 1, (0, 32)),
   "512": (512, 512, 32, 1, None),
+  "hd8": (1920, 1080, 32, 8, None),
+  "hd16": (1920, 1080, 32, 16, None),
+  "hd32": (1920, 1080, 32, 32, None),
+  "4k128/2": (3840, 2160, 128, 1, (0, 64)),
+  "4k128/4": (3840, 2160, 128, 1, (0, 32)),
+  "8k256": (8192, 8192, 256, 1, None),
 }
 def run(name, reps=5, kernel="auto"):
     W, H, B, F, br = WL[name]
@@ -32,16 +38,20 @@ def run(name, reps=5, kernel="auto"):
     ms = s.elapsed_time(e) / reps
     alg = F * (H * W + 256 + 4 * nb * H * W)
     return ms, alg / ms / 1e6
-res = []
-names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(WL)
-for name in names:
-    for kern in ("auto", "crossweave"):
-        if kern == "crossweave":
-            for k in ("IH_ROWS_PER_BATCH", "IH_TARGET_WARPS"): os.environ.pop(k, None)
-            ms, gbs = run(name, kernel=kern)
-            print(json.dumps({"wl": name, "kernel": kern, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)
-            continue
-        for R, tw in itertools.product((1, 2, 4), (148 * 16, 148 * 32, 148 * 64)):
-            os.environ["IH_ROWS_PER_BATCH"] = str(R); os.environ["IH_TARGET_WARPS"] = str(tw)
-            ms, gbs = run(name)
-            print(json.dumps({"wl": name, "R": R, "tw": tw, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)
+def main():
+  names = sys.argv[1].split(",") if len(sys.argv) > 1 else list(WL)
+  for name in names:
+      for kern in ("auto", "crossweave"):
+          if kern == "crossweave":
+              for k in ("IH_ROWS_PER_BATCH", "IH_TARGET_WARPS"): os.environ.pop(k, None)
+              ms, gbs = run(name, kernel=kern)
+              print(json.dumps({"wl": name, "kernel": kern, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)
+              continue
+          for R, tw in itertools.product((1, 2, 4), (148 * 16, 148 * 32, 148 * 64)):
+              os.environ["IH_ROWS_PER_BATCH"] = str(R); os.environ["IH_TARGET_WARPS"] = str(tw)
+              ms, gbs = run(name)
+              print(json.dumps({"wl": name, "R": R, "tw": tw, "ms": round(ms, 4), "GBs": round(gbs, 1), "frac": round(gbs / PEAK, 3)}), flush=True)
+
+
+if __name__ == "__main__" and os.environ.get("SWEEP_ONE") is None:
+    main()

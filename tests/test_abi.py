@@ -94,11 +94,13 @@ def test_window_and_region_validation():
 
 def test_workspace_plan():
     L = _native.lib()
-    # a large batch needs no segment carries -> no workspace
-    assert L.ih_workspace_bytes(64, 1080, 1920, 32, 0) == 0
-    # a single HD frame is split into row segments -> (nseg, nbp, Wp) u32 table
-    n = L.ih_workspace_bytes(1, 1080, 1920, 32, 0)
-    assert n > 0 and n % (32 * 1920 * 4) == 0
+    # frames are split into row segments until ~4 waves of CTAs exist; the
+    # carry table is (frames, nseg, nbp, Wp) u16
+    for frames in (1, 8, 64):
+        n = L.ih_workspace_bytes(frames, 1080, 1920, 32, 0)
+        assert n > 0 and n % (frames * 32 * 1920 * 2) == 0
+    # tiny problems with few rows need no carries
+    assert L.ih_workspace_bytes(1, 40, 64, 4, 0) == 0
     # cross-weave needs none; too-wide images fall back to cross-weave under auto
     assert L.ih_workspace_bytes(1, 1080, 1920, 32, _native.KERNEL_CROSSWEAVE) == 0
     assert L.ih_workspace_bytes(1, 16, 20000, 8, 0) == 0

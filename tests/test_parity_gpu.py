@@ -25,7 +25,8 @@ def crc_of(t) -> str:
 
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
-    for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA"):
+    for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -100,7 +101,8 @@ SHAPES = [(1, 1), (1, 193), (193, 1), (7, 131), (61, 257), (128, 128), (96, 500)
 @pytest.mark.parametrize("nseg", [0, 2, 3, 7])
 @pytest.mark.parametrize("rows_per_batch", [1, 2, 4])
 @pytest.mark.parametrize("tma", [True, False])
-def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch, tma):
+@pytest.mark.parametrize("carry", ["lookback", "table_sum", "table_prefix"])
+def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch, tma, carry):
     """Force K2 row segmentation (colcounts/colprefix/carry-init path), every
     barrier batch size, and both input paths (TMA smem ring / LDG); compare
     with the oracle bit for bit."""
@@ -109,6 +111,10 @@ def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch, tma):
     monkeypatch.setenv("IH_ROWS_PER_BATCH", str(rows_per_batch))
     if not tma:
         monkeypatch.setenv("IH_NO_TMA", "1")
+    if carry == "lookback":
+        monkeypatch.setenv("IH_CARRY_LOOKBACK", "1")
+    elif carry == "table_prefix":
+        monkeypatch.setenv("IH_TABLE_SUM_MAX", "1")  # always run k2_colprefix
     for (h, w) in SHAPES:
         bins = int(rng.choice([1, 3, 5, 16, 64]))
         px = rng.integers(0, 256, (h, w), dtype=np.uint8)
@@ -117,13 +123,28 @@ def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch, tma):
         assert np.array_equal(got, O.compute_crossweave(px, lut, bins)), (h, w, bins)
 
 
-def test_auto_segmentation_sizes(rng):
+@pytest.mark.parametrize("nseg", [0, 40, 200])
+@pytest.mark.parametrize("lookback", [False, True])
+def test_auto_segmentation_sizes(monkeypatch, rng, nseg, lookback):
+    """Real sizes with many segments (look-back chains up to 200 long)."""
+    if nseg:
+        monkeypatch.setenv("IH_NSEG", str(nseg))
+    if lookback:
+        monkeypatch.setenv("IH_CARRY_LOOKBACK", "1")
     for (h, w) in [(1080, 1920), (2160, 640), (500, 64)]:
         for bins in (1, 4, 32):
             px = rng.integers(0, 256, (h, w), dtype=np.uint8)
             lut = O.np_uniform_table(bins)
             got = dev_compute(px, lut, bins).cpu().numpy()
             assert np.array_equal(got, O.compute_crossweave(px, lut, bins)), (h, w, bins)
+
+
+def test_tall_image_sum_mode(rng):
+    """H > 65535: u16 prefixes impossible, the scan sums 16-bit count slots."""
+    px = rng.integers(0, 256, (70001, 5), dtype=np.uint8)
+    lut = O.np_uniform_table(3)
+    got = dev_compute(px, lut, 3).cpu().numpy()
+    assert np.array_equal(got, O.compute_crossweave(px, lut, 3))
 
 
 def test_unaligned_rows_and_odd_widths(rng):
