@@ -211,8 +211,8 @@ def run_ours(args, rank, world, local_rank):
         ev_mid.record(stream)
         device.scan(d_frames, spec.table, BINS, out, stream=stream)
 
-    ws_bytes = device.workspace_bytes(nloc, HEIGHT, WIDTH, BINS)
-    launches_per_step = 1 + (2 if ws_bytes > 0 else 0)
+    plan = device.plan(nloc, HEIGHT, WIDTH, BINS, aligned16=d_frames.data_ptr() % 16 == 0)
+    launches_per_step = plan["launches"]
 
     def barrier():
         if world > 1:
@@ -288,6 +288,7 @@ def run_ours(args, rank, world, local_rank):
                      "alg_bytes_per_launch": nloc * ALG_BYTES_PER_HIST,
                      "launch_ms": scan_ms, "prepare_ms": prep_ms},
         "gpu_launches": launches_per_step * args.steps,
+        "plan": plan,
         "parity": "frame 0 crc32 == reference golden" if not bad else "MISMATCH",
         "clocks": clocks.summary(),
     }

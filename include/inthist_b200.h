@@ -96,6 +96,17 @@ ih_status ih_ih_scan(const uint8_t *img, int64_t frames, int64_t height, int64_t
                      int32_t bins, int32_t bin_lo, int32_t bin_hi, uint32_t *out,
                      void *workspace, size_t workspace_bytes, int32_t kernel, void *stream);
 
+/* The execution plan ih_integral_histogram would use for this problem
+ * (diagnostics and benchmark bookkeeping; no device work).  `aligned16` says
+ * whether image rows are 16-byte aligned (the TMA path).  On return:
+ *   info[0] kernel family used (ih_kernel)   info[1] kernel launches per call
+ *   info[2] row segments per frame           info[3] rows per segment
+ *   info[4] 128-column chunks per lane       info[5] rows per barrier batch
+ *   info[6] warps per CTA                    info[7] workspace bytes needed
+ * Same shape/parameter errors as ih_integral_histogram. */
+ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
+                           int32_t kernel, int32_t aligned16, int64_t *info);
+
 /* Batched four-corner region queries (core.py:179-195).
  *   t        device (nb, height, width) uint32 integral histogram (a slab is fine)
  *   regions  device (Q, 4) int32 rows (r0, c0, r1, c1), inclusive (core.py:131-158)

@@ -139,15 +139,28 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   p.ngroups = (nb + ih::kGroup - 1) / ih::kGroup;
   p.nbp = p.ngroups * ih::kGroup;
   p.carry = ih::CARRY_TABLE;  // for the occupancy query; fixed up below
-  // Row segments: enough CTAs for ~4 waves of resident CTAs (measured best for
-  // every frame-batch / single-image class in scripts/sweep*.py); each extra
-  // segment costs a u16 count slot of 1/(2S) of the output, mostly in L2.
-  const double waves = env_int("IH_TARGET_WAVES_X10", 40) / 10.0;
+  // Row segments (measured, scripts/sweep2.py -> profiles/r01_sweep_*.jsonl):
+  // every CTA does the same work, so the CTA count should be a whole number
+  // of "waves" of resident CTAs; ~4 waves when frames x groups fill at least a
+  // quarter wave, ~2 waves (8 for the 1024-thread variant) otherwise.  If
+  // the minimum segment height caps the count, snap down to whole waves.
+  // Each segment costs a u16 count slot of 1/(2S) of the output (mostly L2).
   const int64_t slots = (int64_t)kNumSMs * ctas_per_sm(p);
-  const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", 48);
   const int64_t units = frames * p.ngroups;
-  int64_t nseg = (int64_t)(waves * slots / units + 0.999);
+  const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", 32);
   const int64_t max_seg = (H + min_rows - 1) / min_rows;
+  const bool many = units * 4 >= slots;  // >= a quarter wave without segments
+  double waves = many ? 4.0 : (p.big ? 8.0 : 2.0);
+  const int64_t w_env = env_int("IH_TARGET_WAVES_X10", 0);
+  if (w_env > 0) waves = w_env / 10.0;
+  const double raw = waves * (double)slots / (double)units;
+  int64_t nseg;
+  if (raw <= (double)max_seg) {
+    nseg = many ? (int64_t)(raw + 0.999) : (int64_t)(raw + 0.5);
+  } else {
+    const int64_t whole = max_seg * units / slots;  // whole waves that fit under the cap
+    nseg = whole >= 1 ? whole * slots / units : max_seg;
+  }
   if (nseg > max_seg) nseg = max_seg;
   if (nseg > 65535) nseg = 65535;
   if (nseg < 1) nseg = 1;
@@ -436,6 +449,37 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   ih::k4_window_counts<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       t, nb, height, width, h, w, reinterpret_cast<long long*>(out));
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts");
+  return IH_OK;
+}
+
+ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
+                           int32_t kernel, int32_t aligned16, int64_t* info) {
+  if (frames < 1 || height < 1 || width < 1) return fail(IH_ERR_SHAPE, "image must be non-empty");
+  if (slab_bins < 1 || slab_bins > 256) return fail(IH_ERR_SHAPE, "bin count must be in [1, 256]");
+  if ((uint64_t)width * (uint64_t)height > 0xffffffffull)
+    return fail(IH_ERR_CAPACITY, "image exceeds the 32-bit count range");
+  if (kernel < IH_KERNEL_AUTO || kernel > IH_KERNEL_CROSSWEAVE)
+    return fail(IH_ERR_PARAM, "unknown kernel");
+  if (!info) return fail(IH_ERR_PARAM, "null info pointer");
+  const bool tma = aligned16 != 0 && env_int("IH_NO_TMA", 0) == 0;
+  K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0, tma);
+  const int k = resolve_kernel(kernel, p);
+  for (int i = 0; i < 8; ++i) info[i] = 0;
+  info[0] = k;
+  if (k == IH_KERNEL_CROSSWEAVE) {
+    info[1] = height > 1 ? 2 : 1;
+    return IH_OK;
+  }
+  if (p.cpl == 0) return fail(IH_ERR_PARAM, "single-pass kernel supports width <= 8192");
+  int launches = 1;
+  if (p.carry == ih::CARRY_TABLE) launches += table_prefix_h(p, height) ? 2 : 1;
+  info[1] = launches;
+  info[2] = p.nseg;
+  info[3] = p.S;
+  info[4] = p.cpl;
+  info[5] = p.R;
+  info[6] = p.nwarps;
+  info[7] = (int64_t)k2_ws_bytes(frames, p);
   return IH_OK;
 }
 

@@ -38,14 +38,15 @@ namespace ih {
 // ---------------------------------------------------------------------------
 constexpr int kCountSlab = 32;
 constexpr int kCountWarps = 8;
-constexpr size_t kCountSmem = (size_t)kCountWarps * kCountSlab * 4 * 32 * sizeof(uint16_t);
+constexpr int kCountRows = kCountSlab + 1;  // + a dummy row for "no bin in this slab"
+constexpr size_t kCountSmem = (size_t)kCountWarps * kCountRows * 4 * 32 * sizeof(uint16_t);
 
 template <bool ALIGNED>
 __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
     RelLut lut, int S, int nseg, int nbp, int64_t Wp, int nslab, uint16_t* __restrict__ ws) {
-  extern __shared__ __align__(16) uint16_t chist[];  // [warp][bin][k][lane]
-  __shared__ uint8_t slut[512];
+  extern __shared__ __align__(16) uint16_t chist[];  // [warp][bin row][k][lane]
+  __shared__ uint16_t sofs[512];  // pixel -> byte offset of its bin row (dummy row if none)
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t c = (int64_t)blockIdx.x * kChunk + 4 * lane;
@@ -53,9 +54,10 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
   const int slab = blockIdx.z % nslab;
   const int64_t f = blockIdx.z / nslab;
   const uint32_t lo = (uint32_t)slab * kCountSlab;
+  constexpr uint32_t kRowBytes = 4 * 32 * sizeof(uint16_t);  // one bin row: [k][lane]
   for (int v = threadIdx.x; v < 512; v += blockDim.x) {
-    const uint32_t d = v < 256 ? (uint32_t)lut.rel[v] - lo : 0xffu;
-    slut[v] = d < (uint32_t)kCountSlab ? (uint8_t)d : (uint8_t)0xff;
+    const uint32_t d = v < 256 ? (uint32_t)lut.rel[v] - lo : 0xffffffffu;
+    sofs[v] = (uint16_t)((d < (uint32_t)kCountSlab ? d : (uint32_t)kCountSlab) * kRowBytes);
   }
   {
     uint4* z = reinterpret_cast<uint4*>(chist);
@@ -65,7 +67,8 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
 #pragma unroll
   for (int k = 0; k < 4; ++k) inval[k] = (c + k < W) ? 0u : 256u;
   __syncthreads();
-  uint16_t* hist = chist + (size_t)warp * kCountSlab * 4 * 32 + lane;  // [bin][k] stride 32
+  // this lane's counters: byte base + bin-row offset + k * 64
+  char* hbase = reinterpret_cast<char*>(chist + (size_t)warp * kCountRows * 4 * 32 + lane);
   const uint8_t* base = img + f * fstride;
   const int64_t seg0 = (int64_t)s * S;
   const int64_t seg1 = (seg0 + S < H ? seg0 + S : H);
@@ -84,20 +87,26 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
   auto count4 = [&](uint32_t px) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t d = slut[((px >> (8 * k)) & 0xffu) | inval[k]];
-      if (d != 0xffu) hist[(d * 4 + k) * 32] += 1;
+      uint16_t* h = reinterpret_cast<uint16_t*>(
+          hbase + sofs[((px >> (8 * k)) & 0xffu) | inval[k]] + k * 32 * sizeof(uint16_t));
+      *h += 1;
     }
   };
-  if (c < W) {
-    int64_t r = r0;
-    for (; r + 8 <= r1; r += 8) {
-      uint32_t px[8];
+  if (c < W && r0 < r1) {
+    // software pipeline: the next 8 rows' loads are in flight while counting
+    constexpr int U = 8;
+    uint32_t cur[U], nxt[U];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) px[i] = load_px(r + i);
+    for (int i = 0; i < U; ++i) cur[i] = r0 + i < r1 ? load_px(r0 + i) : 0u;
+    for (int64_t r = r0; r < r1; r += U) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) count4(px[i]);
+      for (int i = 0; i < U; ++i) nxt[i] = r + U + i < r1 ? load_px(r + U + i) : 0u;
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+        if (r + i < r1) count4(cur[i]);
+#pragma unroll
+      for (int i = 0; i < U; ++i) cur[i] = nxt[i];
     }
-    for (; r < r1; ++r) count4(load_px(r));
   }
   __syncthreads();
   // sum the 8 private histograms; item = (bin, lane) -> 4 columns, one 8-byte store
@@ -110,7 +119,7 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
     for (int w = 0; w < kCountWarps; ++w)
 #pragma unroll
       for (int k = 0; k < 4; ++k)
-        sum[k] += chist[(size_t)w * kCountSlab * 4 * 32 + (b * 4 + k) * 32 + l];
+        sum[k] += chist[(size_t)w * kCountRows * 4 * 32 + (b * 4 + k) * 32 + l];
     *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) =
         make_uint2(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16));
   }
@@ -451,19 +460,33 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
   } else if (CARRY == CARRY_TABLE && s > 0) {
     const int64_t plane_sz = (int64_t)a.nbp * a.Wp;
     const uint16_t* cp = a.colpre + (f * a.nseg) * plane_sz + (int64_t)g * kGroup * a.Wp;
-    // prefix table: one slot; raw counts: sum slots 0..s-1 here (L2-resident)
-    for (int sp = a.table_is_prefix ? s : 0; sp < (a.table_is_prefix ? s + 1 : s); ++sp) {
-      const uint16_t* q = cp + sp * plane_sz;
+    // prefix table: one slot; raw counts: sum slots 0..s-1 here (L2-resident),
+    // U slots' loads in flight at a time (register budget bounds U)
+    constexpr int U = CPL >= 4 ? 1 : 4;
+    const int sp0 = a.table_is_prefix ? s : 0;
+    const int sp1 = a.table_is_prefix ? s + 1 : s;
+    for (int sp = sp0; sp < sp1; sp += U) {
+      uint2 v[U][CPL][kGroup];
 #pragma unroll
-      for (int k = 0; k < CPL; ++k)
+      for (int u = 0; u < U; ++u)
 #pragma unroll
-        for (int i = 0; i < kGroup; ++i) {
-          const uint2 v = *reinterpret_cast<const uint2*>(q + i * a.Wp + c0[k]);
-          acc[k][0][i] += v.x & 0xffffu;
-          acc[k][1][i] += v.x >> 16;
-          acc[k][2][i] += v.y & 0xffffu;
-          acc[k][3][i] += v.y >> 16;
-        }
+        for (int k = 0; k < CPL; ++k)
+#pragma unroll
+          for (int i = 0; i < kGroup; ++i)
+            v[u][k][i] = sp + u < sp1 ? *reinterpret_cast<const uint2*>(
+                                            cp + (sp + u) * plane_sz + i * a.Wp + c0[k])
+                                      : make_uint2(0u, 0u);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+#pragma unroll
+          for (int i = 0; i < kGroup; ++i) {
+            acc[k][0][i] += v[u][k][i].x & 0xffffu;
+            acc[k][1][i] += v[u][k][i].x >> 16;
+            acc[k][2][i] += v[u][k][i].y & 0xffffu;
+            acc[k][3][i] += v[u][k][i].y >> 16;
+          }
     }
   }
 

@@ -12,6 +12,8 @@ synchronise the host.
 
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 import torch
 
@@ -96,6 +98,21 @@ def _prepare_args(images, table, bins, bin_range, kernel, stream) -> _Args:
 def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto") -> int:
     return int(_native.lib().ih_workspace_bytes(frames, height, width, slab_bins,
                                                 _native.KERNELS[kernel]))
+
+
+PLAN_FIELDS = ("kernel", "launches", "segments", "segment_rows", "chunks_per_lane",
+               "rows_per_batch", "warps_per_cta", "workspace_bytes")
+
+
+def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto",
+         aligned16: bool = True) -> dict:
+    """The launch plan the C ABI would use (ih_plan_describe); no device work."""
+    info = (ctypes.c_int64 * 8)()
+    _native.check(_native.lib().ih_plan_describe(frames, height, width, slab_bins,
+                                                 _native.KERNELS[kernel], int(aligned16), info))
+    d = dict(zip(PLAN_FIELDS, list(info)))
+    d["kernel"] = {v: k for k, v in _native.KERNELS.items()}[d["kernel"]]
+    return d
 
 
 def empty_output(frames: int, slab_bins: int, height: int, width: int, device) -> torch.Tensor:
