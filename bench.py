@@ -265,6 +265,18 @@ def run_ours(args, rank, world, local_rank):
                "d2h_bytes_per_step": int(pipe.d2h_bytes) * world,
                "steps": args.e2e_steps, "timer": "host perf_counter around synchronized steps"}
         crc_ok = crc_ok and f"{zlib.crc32(h_out[0].numpy().tobytes()):08x}" == gold[f0]
+        # the e2e roofline: a plain pinned D2H copy of one output slice (PCIe bound)
+        probe = out[: min(nloc, 4)].view(torch.int32)
+        dst = h_out[: probe.shape[0]].view(torch.int32)
+        torch.cuda.synchronize(dev)
+        t1 = time.perf_counter()
+        for _ in range(3):
+            dst.copy_(probe, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        d2h_gbs = 3 * probe.numel() * 4 / (time.perf_counter() - t1) / 1e9
+        e2e["d2h_copy_gbs"] = d2h_gbs
+        e2e["e2e_out_gbs"] = e2e["value"] * OUT_BYTES_PER_HIST / 1e9 / world
+        e2e["frac_of_d2h_copy"] = e2e["e2e_out_gbs"] / d2h_gbs
         del h_out, h_in, pipe
 
     total_ms, scan_ms, prep_ms, bad = reduce_max([total_ms, scan_ms, prep_ms,
