@@ -155,7 +155,24 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (w_env > 0) waves = w_env / 10.0;
   const double raw = waves * (double)slots / (double)units;
   int64_t nseg;
-  if (raw <= (double)max_seg) {
+  if (raw <= (double)max_seg && slots == kNumSMs) {
+    // one CTA per SM: a partial last wave idles whole SMs for a CTA's
+    // lifetime; pick the count in [raw/2, 2*raw] that leaves the fewest idle
+    // slots (ties: fewer segments)
+    int64_t best = 1;
+    double best_idle = 2.0;
+    const int64_t lo = (int64_t)(raw / 2) > 1 ? (int64_t)(raw / 2) : 1;
+    const int64_t hi = (int64_t)(2 * raw) < max_seg ? (int64_t)(2 * raw) : max_seg;
+    for (int64_t n = lo; n <= hi; ++n) {
+      const double w = (double)(units * n) / (double)slots;
+      const double idle = ((double)(int64_t)(w + 0.999999) - w) / (double)(int64_t)(w + 0.999999);
+      if (idle < best_idle - 0.02) {
+        best_idle = idle;
+        best = n;
+      }
+    }
+    nseg = best;
+  } else if (raw <= (double)max_seg) {
     nseg = many ? (int64_t)(raw + 0.999) : (int64_t)(raw + 0.5);
   } else {
     const int64_t whole = max_seg * units / slots;  // whole waves that fit under the cap
@@ -427,9 +444,8 @@ ih_status ih_region_histograms(const uint32_t* t, int32_t nb, int64_t height, in
   if (q == 0) return IH_OK;
   if (!t || !regions || !out) return fail(IH_ERR_PARAM, "null pointer");
   if ((uintptr_t)regions % 16 != 0) return fail(IH_ERR_PARAM, "regions must be 16-byte aligned");
-  const int64_t total = q * nb;
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > kNumSMs * 32) blocks = kNumSMs * 32;
+  int64_t blocks = (q + 7) / 8;  // 8 warps per CTA, one query per warp
+  if (blocks > kNumSMs * 64) blocks = kNumSMs * 64;
   ih::k3_region_histograms<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       t, nb, height, width, reinterpret_cast<const int4*>(regions), q,
       reinterpret_cast<unsigned long long*>(out));
@@ -443,10 +459,10 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   if (h > height || w > width) return fail(IH_ERR_BOUNDS, "window exceeds image");
   if (nb < 1) return fail(IH_ERR_SHAPE, "tensor must be non-empty");
   if (!t || !out) return fail(IH_ERR_PARAM, "null pointer");
-  const int64_t total = (int64_t)nb * (height - h + 1) * (width - w + 1);
-  int64_t blocks = (total + 255) / 256;
-  if (blocks > kNumSMs * 32) blocks = kNumSMs * 32;
-  ih::k4_window_counts<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+  if (nb > 65535) return fail(IH_ERR_PARAM, "too many bins");
+  const int64_t R = height - h + 1, C = width - w + 1;
+  dim3 grid((unsigned)((C + 511) / 512), (unsigned)(R < 65535 ? R : 65535), (unsigned)nb);
+  ih::k4_window_counts<<<grid, 256, 0, (cudaStream_t)stream>>>(
       t, nb, height, width, h, w, reinterpret_cast<long long*>(out));
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts");
   return IH_OK;

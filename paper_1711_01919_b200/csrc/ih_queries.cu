@@ -8,48 +8,75 @@
 
 namespace ih {
 
-// Thread per (query, bin); bin fastest so the (Q, nb) u64 output is coalesced.
+// K3: one warp per query (grid-stride over queries), lanes over bins: the
+// (Q, nb) u64 output row of a query is written coalesced, and each lane keeps
+// 4 corners x 4 bins = 16 independent gathers in flight (the reads are random
+// by nature: 4 corners per bin plane, planes H*W*4 bytes apart).
 __global__ void __launch_bounds__(256) k3_region_histograms(const uint32_t* __restrict__ t, int nb,
                                                              int64_t H, int64_t W,
                                                              const int4* __restrict__ regions,
                                                              int64_t Q,
                                                              unsigned long long* __restrict__ out) {
-  const int64_t total = Q * nb;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t q = i / nb;
-    const int b = (int)(i % nb);
-    const int4 rg = __ldg(regions + q);  // r0, c0, r1, c1 (inclusive)
-    const uint32_t* p = t + (int64_t)b * H * W;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+  const int64_t plane = H * W;
+  for (int64_t q = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); q < Q;
+       q += warps) {
+    const int4 rg = __ldg(regions + q);  // r0, c0, r1, c1 (inclusive), warp-uniform
     const int64_t r0 = rg.x, c0 = rg.y, r1 = rg.z, c1 = rg.w;
-    int64_t v = (int64_t)__ldg(p + r1 * W + c1);
-    if (r0 > 0) v -= (int64_t)__ldg(p + (r0 - 1) * W + c1);
-    if (c0 > 0) v -= (int64_t)__ldg(p + r1 * W + (c0 - 1));
-    if (r0 > 0 && c0 > 0) v += (int64_t)__ldg(p + (r0 - 1) * W + (c0 - 1));
-    out[i] = (unsigned long long)v;
+    const bool top = r0 > 0, left = c0 > 0;
+    const int64_t o11 = r1 * W + c1;
+    const int64_t o01 = top ? (r0 - 1) * W + c1 : 0;
+    const int64_t o10 = left ? r1 * W + (c0 - 1) : 0;
+    const int64_t o00 = top && left ? (r0 - 1) * W + (c0 - 1) : 0;
+    unsigned long long* orow = out + q * nb;
+    for (int b0 = 0; b0 < nb; b0 += 128) {
+      uint32_t v[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = b0 + u * 32 + lane;
+        const uint32_t* p = t + (int64_t)(b < nb ? b : 0) * plane;
+        v[u][0] = b < nb ? __ldg(p + o11) : 0u;
+        v[u][1] = b < nb && top ? __ldg(p + o01) : 0u;
+        v[u][2] = b < nb && left ? __ldg(p + o10) : 0u;
+        v[u][3] = b < nb && top && left ? __ldg(p + o00) : 0u;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int b = b0 + u * 32 + lane;
+        if (b < nb)
+          orow[b] = (unsigned long long)((int64_t)v[u][0] - (int64_t)v[u][1] - (int64_t)v[u][2] +
+                                         (int64_t)v[u][3]);
+      }
+    }
   }
 }
 
-// Thread per output element (b, i, j), j fastest: the four corner rows are
-// read coalesced; corners above row 0 / left of column 0 are zero
-// (likelihood.py:44-51).
+// K4: grid (column blocks, output rows, bins); thread per output element, two
+// per thread (j and j + blockDim.x).  The four corner rows are read coalesced;
+// corners above row 0 / left of column 0 are zero (likelihood.py:44-51).
 __global__ void __launch_bounds__(256) k4_window_counts(const uint32_t* __restrict__ t, int nb,
                                                          int64_t H, int64_t W, int h, int w,
                                                          long long* __restrict__ out) {
   const int64_t R = H - h + 1, C = W - w + 1;
-  const int64_t total = (int64_t)nb * R * C;
-  for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t b = idx / (R * C);
-    const int64_t rem = idx % (R * C);
-    const int64_t i = rem / C, j = rem % C;
-    const uint32_t* p = t + b * H * W;
-    const int64_t rb = i + h - 1, cr = j + w - 1;
-    long long v = (long long)__ldg(p + rb * W + cr);
-    if (i > 0) v -= (long long)__ldg(p + (i - 1) * W + cr);
-    if (j > 0) v -= (long long)__ldg(p + rb * W + (j - 1));
-    if (i > 0 && j > 0) v += (long long)__ldg(p + (i - 1) * W + (j - 1));
-    out[idx] = v;
+  const int64_t b = blockIdx.z;
+  const uint32_t* p = t + b * H * W;
+  for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
+    const uint32_t* bot = p + (i + h - 1) * W;
+    const uint32_t* topr = p + (i - 1) * W;  // used only when i > 0
+    long long* orow = out + (b * R + i) * C;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      const int64_t j = ((int64_t)blockIdx.x * 2 + half) * blockDim.x + threadIdx.x;
+      if (j >= C) continue;
+      long long v = (long long)__ldg(bot + j + w - 1);
+      if (j > 0) v -= (long long)__ldg(bot + j - 1);
+      if (i > 0) {
+        v -= (long long)__ldg(topr + j + w - 1);
+        if (j > 0) v += (long long)__ldg(topr + j - 1);
+      }
+      __stcs(orow + j, v);
+    }
   }
 }
 

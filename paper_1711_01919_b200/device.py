@@ -128,7 +128,7 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
     bins [lo, hi) of ``bin_range`` (default: all).  Bit-identical to every
     reference strategy (strategies.py:109-229).
     """
-    squeeze = images.dim() == 2
+    squeeze = images.dim() == 2 and out is None
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
     nb = a.hi - a.lo
     if nb < 1 or a.lo < 0 or a.hi > a.bins:

@@ -327,3 +327,45 @@ def test_native_library_is_the_one_loaded():
 
     maps = open(f"/proc/{os.getpid()}/maps").read()
     assert _native.LIB_PATH in maps
+
+
+@pytest.mark.parametrize("frames,h,w,bins", [(4, 270, 480, 32), (1, 1080, 1920, 32), (2, 100, 3000, 17)])
+def test_cuda_graph_capture_and_streams(frames, h, w, bins, rng):
+    """The whole call (row-segment prepass + scan) is stream-ordered and
+    graph-capturable: capture once on a side stream, replay with new pixels."""
+    lut = O.np_uniform_table(bins)
+    imgs = torch.from_numpy(rng.integers(0, 256, (frames, h, w), dtype=np.uint8)).cuda()
+    out = device.empty_output(frames, bins, h, w, imgs.device)
+    device.integral_histogram(imgs, lut, bins, out=out)  # warm-up: workspace, attributes
+    torch.cuda.synchronize()
+    side = torch.cuda.Stream()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=side):
+        device.integral_histogram(imgs, lut, bins, out=out)
+    for _ in range(2):
+        new = rng.integers(0, 256, (frames, h, w), dtype=np.uint8)
+        imgs.copy_(torch.from_numpy(new))
+        g.replay()
+        torch.cuda.synchronize()
+        for f in range(frames):
+            assert np.array_equal(out[f].cpu().numpy(), O.compute_crossweave(new[f], lut, bins))
+
+
+def test_plan_describe_matches_launches():
+    p = device.plan(64, 1080, 1920, 32)
+    assert p["kernel"] == "single_pass" and p["launches"] in (1, 2, 3)
+    assert p["segments"] * p["segment_rows"] >= 1080
+    assert device.plan(1, 4, 20000, 8)["kernel"] == "crossweave"
+    assert device.workspace_bytes(64, 1080, 1920, 32) >= p["workspace_bytes"]
+
+
+def test_out_argument_and_int32_view(rng):
+    px = rng.integers(0, 256, (50, 70), dtype=np.uint8)
+    lut = O.np_uniform_table(5)
+    out = torch.zeros((1, 5, 50, 70), dtype=torch.int32, device="cuda")
+    res = device.integral_histogram(device.upload_image(px), lut, 5, out=out)
+    assert res is out
+    assert np.array_equal(out[0].cpu().numpy().view(np.uint32), O.compute_crossweave(px, lut, 5))
+    with pytest.raises(ih.ShapeError):
+        device.integral_histogram(device.upload_image(px), lut, 5,
+                                  out=torch.zeros((1, 4, 50, 70), dtype=torch.int32, device="cuda"))
