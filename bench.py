@@ -2,18 +2,22 @@
 """Benchmark: integral histograms/s and output GB/s (% of HBM) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload hd64|4k128|8k256] [--gather]
 
-Workload (BASELINE.json configs[2], the north-star's 70 % target config):
-1920x1080 uint8 frames, 32 uniform bins, a batch of 64 frames per step,
-frame-sharded across the N ranks (strong scaling: 64 frames in total).
-Synthetic frames are ``synth_image(1920, 1080, k)`` for k = 0..63 (the
-reference bench's generator, bench.py:59-62).
+Default workload (BASELINE.json configs[2], the north-star's 70 % target
+config): 1920x1080 uint8 frames, 32 uniform bins, a batch of 64 frames per
+step, frame-sharded across the N ranks (strong scaling: 64 frames in total).
+`4k128` / `8k256` are configs[3] / configs[4]: one image per step, the bin
+dimension sharded across ranks (each rank computes a contiguous bin slab, no
+collective on the data path; `--gather` additionally times an NCCL gather of
+the slabs onto rank 0, reported separately).  Synthetic images are
+``synth_image(W, H, k)`` (the reference bench's generator, bench.py:59-62).
 
-One JSON line on rank 0.  ``value`` is device-resident throughput (frames
-already in HBM, outputs written to HBM), CUDA-event timed, max over ranks;
-``e2e`` is the same metric through the host-buffer public API
-(pipeline.FramePipeline: pinned H2D of the frames, kernels, pinned D2H of
-the 17 GB result, all inside the timed region).
+One JSON line on rank 0.  ``value`` is device-resident throughput (images in
+HBM, outputs written to HBM), CUDA-event timed, max over ranks; ``e2e`` is the
+same metric through the host-buffer public API (pipeline.FramePipeline: pinned
+H2D of the images, kernels, pinned D2H of the whole result, all inside the
+timed region).
 
 ``--impl reference`` times the reference algorithm on the host CPU: the
 oracle's C port of the reference's fastest strategy, cross-weave
@@ -30,18 +34,46 @@ import statistics
 import sys
 import threading
 import time
+import zlib
+from dataclasses import dataclass
 
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-WIDTH, HEIGHT, BINS, FRAMES = 1920, 1080, 32, 64
-WORKLOAD = "1920x1080 u8 frames, 32 uniform bins, 64-frame batch (BASELINE cfg2), frame-sharded"
 METRIC = "integral histograms/sec"
 UNIT = "hist/s"
-ALG_BYTES_PER_HIST = WIDTH * HEIGHT + 256 + 4 * BINS * WIDTH * HEIGHT
-OUT_BYTES_PER_HIST = 4 * BINS * WIDTH * HEIGHT
+
+
+@dataclass(frozen=True)
+class Workload:
+    key: str
+    width: int
+    height: int
+    bins: int
+    frames: int  # integral histograms per step
+    shard: str   # "frames" | "bins"
+    desc: str
+
+    @property
+    def alg_bytes(self) -> int:  # u8 read + LUT + u32 write, one full histogram
+        return self.width * self.height + 256 + 4 * self.bins * self.width * self.height
+
+    @property
+    def out_bytes(self) -> int:
+        return 4 * self.bins * self.width * self.height
+
+
+WORKLOADS = {
+    "hd64": Workload("hd64", 1920, 1080, 32, 64, "frames",
+                     "1920x1080 u8 frames, 32 uniform bins, 64-frame batch (BASELINE cfg2), "
+                     "frame-sharded"),
+    "4k128": Workload("4k128", 3840, 2160, 128, 1, "bins",
+                      "3840x2160 u8 image, 128 uniform bins (BASELINE cfg3), bin-sharded"),
+    "8k256": Workload("8k256", 8192, 8192, 256, 1, "bins",
+                      "8192x8192 u8 image, 256 uniform bins (BASELINE cfg4), bin-sharded"),
+}
 
 
 def synth_image(width, height, seed):
@@ -50,25 +82,33 @@ def synth_image(width, height, seed):
     return rng.integers(0, 256, size=(height, width), dtype=np.uint8)
 
 
+def uniform_table(bins):
+    return ((np.arange(256) * bins) // 256).astype(np.uint8)
+
+
 def measured_peaks():
-    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     try:
-        with open(path) as fh:
-            d = json.load(fh)
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return float(json.load(fh)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def committed_traffic():
-    """dram__bytes_read.sum + dram__bytes_write.sum per k2_scan launch from the
-    committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+def committed_traffic(wl: Workload):
+    """dram__bytes_read.sum + dram__bytes_write.sum per histogram of k2_scan from
+    the committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    if wl.key != "hd64":
+        return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            d = json.load(fh)
-        return d.get("k2_scan_hd_bytes_per_frame")
+            return json.load(fh).get("k2_scan_hd_bytes_per_frame")
     except Exception:
         return None
+
+
+def golden():
+    with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as fh:
+        return json.load(fh)
 
 
 class ClockSampler:
@@ -104,16 +144,16 @@ class ClockSampler:
                     self.reasons.add(name)
             self._stop.wait(0.005)
 
-    def __enter__(self):
-        self.thread = threading.Thread(target=self._safe_run, daemon=True)
-        self.thread.start()
-        return self
-
     def _safe_run(self):
         try:
             self._run()
         except Exception as exc:  # NVML missing: report, do not fail the bench
             self.error = repr(exc)
+
+    def __enter__(self):
+        self.thread = threading.Thread(target=self._safe_run, daemon=True)
+        self.thread.start()
+        return self
 
     def __exit__(self, *exc):
         self._stop.set()
@@ -127,68 +167,83 @@ class ClockSampler:
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
 
 
-def cpu_reference_sample(frames_idx, threads=0):
-    """Oracle C port of the reference cross-weave on the host; returns seconds
-    and the number of histograms computed."""
-    from oracle import oracle as O
-
-    lut = O.np_uniform_table(BINS)
-    imgs = [synth_image(WIDTH, HEIGHT, k) for k in frames_idx]
-    t0 = time.perf_counter()
-    for img in imgs:
-        O.compute_crossweave(img, lut, BINS, threads)
-    return time.perf_counter() - t0, len(imgs)
-
-
-def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm on the host CPU (rank 0 only)."""
-    if rank != 0:
-        return
+# ------------------------------------------------------------------ CPU side
+def cpu_sample(wl: Workload, budget_s: float = 20.0):
+    """The oracle's C port of the reference cross-weave on all host threads, on a
+    bounded sample of the workload.  Returns (hist/s, cores, sample text)."""
     from oracle import oracle as O
 
     cores = O.max_threads()
-    per_step = args.ref_frames
-    idx = list(range(per_step))
+    lut = uniform_table(wl.bins)
+    if wl.shard == "frames":
+        # size the sample from one timed frame so it stays within the budget
+        first = synth_image(wl.width, wl.height, 0)
+        t1 = time.perf_counter()
+        O.compute_crossweave(first, lut, wl.bins)
+        per = max(time.perf_counter() - t1, 1e-6)
+        n = int(max(1, min(wl.frames, budget_s / per)))
+        imgs = [synth_image(wl.width, wl.height, k) for k in range(n)]
+        t1 = time.perf_counter()
+        for img in imgs:
+            O.compute_crossweave(img, lut, wl.bins)
+        dt = time.perf_counter() - t1
+        return n / dt, cores, (f"{n} of the {wl.frames} frames (seeds 0..{n - 1}), C port of "
+                               f"reference compute_crossweave (strategies.py:129-150), "
+                               f"{cores} threads")
+    # one big image: time a 16-bin slab (the LUT maps every other bin out of range)
+    img = synth_image(wl.width, wl.height, 0)
+    nb = min(16, wl.bins)
+    slab_lut = np.where(lut < nb, lut, 255).astype(np.uint8)
+    t1 = time.perf_counter()
+    O.compute_crossweave(img, slab_lut, nb)
+    dt = time.perf_counter() - t1
+    return (nb / wl.bins) / dt, cores, (
+        f"bins 0..{nb - 1} of the {wl.bins}-bin tensor of synth_image seed 0, scaled by "
+        f"{nb}/{wl.bins}; C port of reference compute_crossweave, {cores} threads")
+
+
+def config_block(wl: Workload, world: int):
+    return {"workload": wl.desc, "key": wl.key, "width": wl.width, "height": wl.height,
+            "bins": wl.bins, "histograms_per_step": wl.frames,
+            "parallelism": f"{'frame' if wl.shard == 'frames' else 'bin'}-shard x{world}",
+            "l2": f"no flush: per-step output {wl.frames * wl.out_bytes / 1e9:.1f} GB >> 126 MB L2"}
+
+
+def run_reference(args, wl: Workload, rank, world):
+    """--impl reference: the reference algorithm on the host CPU (rank 0 only)."""
+    if rank != 0:
+        return
     for _ in range(args.warmup):
-        cpu_reference_sample(idx[:1])
-    times = []
-    for _ in range(args.steps):
-        dt, n = cpu_reference_sample(idx)
-        times.append(dt)
-    total = sum(times)
-    value = per_step * args.steps / total
-    sample = (f"{per_step} of the 64 HD frames per step (seeds 0..{per_step - 1}), "
-              f"C port of reference compute_crossweave (strategies.py:129-150), {cores} threads")
+        cpu_sample(wl, budget_s=0.2)
+    budget = min(args.ref_budget, 150.0 / args.steps)  # whole run within a few minutes
+    samples = [cpu_sample(wl, budget_s=budget) for _ in range(args.steps)]
+    value = statistics.median(v for v, _, _ in samples)
+    _, cores, sample = samples[0]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
-        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * wl.frames / value,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
-        "data": "synthetic", "config": config_block(world),
+        "data": "synthetic", "config": config_block(wl, world),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
                          "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "output_gbs": value * OUT_BYTES_PER_HIST / 1e9,
+        "output_gbs": value * wl.out_bytes / 1e9,
     }
     print(json.dumps(line), flush=True)
 
 
-def config_block(world):
-    return {"workload": WORKLOAD, "width": WIDTH, "height": HEIGHT, "bins": BINS,
-            "frames_per_step": FRAMES, "parallelism": f"frame-shard x{world}",
-            "l2": "no flush: per-step output 17 GB >> 126 MB L2 (inputs 133 MB > L2)"}
-
-
-def run_ours(args, rank, world, local_rank):
+# ------------------------------------------------------------------ GPU side
+def run_ours(args, wl: Workload, rank, world, local_rank):
     import torch
     import torch.distributed as dist
 
     import paper_1711_01919_b200 as ih
-    from paper_1711_01919_b200 import device, pipeline, sharding
+    from paper_1711_01919_b200 import device, sharding
 
     dev_index = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(dev_index)
     dev = torch.device("cuda", dev_index)
-    spec = ih.BinSpec.uniform(BINS)
+    spec = ih.BinSpec.uniform(wl.bins)
 
     def reduce_max(vals):
         """Max over ranks (NCCL needs CUDA tensors; gloo is used only for the
@@ -199,31 +254,39 @@ def run_ours(args, rank, world, local_rank):
         t = torch.tensor(list(vals), dtype=torch.float64, device=on)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.tolist()
-    f0, f1 = sharding.frame_shards(FRAMES, world)[rank]
-    nloc = f1 - f0
-    host_frames = np.stack([synth_image(WIDTH, HEIGHT, k) for k in range(f0, f1)])
-    d_frames = torch.from_numpy(host_frames).to(dev)
-    out = device.empty_output(nloc, BINS, HEIGHT, WIDTH, dev)
-    stream = torch.cuda.current_stream(dev)
-
-    def step():
-        device.prepare(d_frames, spec.table, BINS, stream=stream)
-        ev_mid.record(stream)
-        device.scan(d_frames, spec.table, BINS, out, stream=stream)
-
-    plan = device.plan(nloc, HEIGHT, WIDTH, BINS, aligned16=d_frames.data_ptr() % 16 == 0)
-    launches_per_step = plan["launches"]
 
     def barrier():
         if world > 1:
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    ev_mid = torch.cuda.Event(enable_timing=True)
-    for _ in range(args.warmup):
-        step()
-    barrier()
+    # this rank's share: frames [f0, f1) x bins [b0, b1)
+    if wl.shard == "frames":
+        f0, f1 = sharding.frame_shards(wl.frames, world)[rank]
+        b0, b1 = 0, wl.bins
+    else:
+        f0, f1 = 0, wl.frames
+        b0, b1 = sharding.bin_slabs(wl.bins, world)[rank]
+    nloc, nb = f1 - f0, b1 - b0
+    active = nloc > 0 and nb > 0
+    host = np.stack([synth_image(wl.width, wl.height, k) for k in range(f0, max(f1, f0 + 1))])
+    d_img = torch.from_numpy(host).to(dev)
+    out = device.empty_output(max(nloc, 1), max(nb, 1), wl.height, wl.width, dev)
+    stream = torch.cuda.current_stream(dev)
+    brange = (b0, b1) if active else None
+    plan = device.plan(nloc, wl.height, wl.width, nb,
+                       aligned16=d_img.data_ptr() % 16 == 0) if active else {"launches": 0}
 
+    def step(ev_mid):
+        if active:
+            device.prepare(d_img, spec.table, wl.bins, bin_range=brange, stream=stream)
+        ev_mid.record(stream)
+        if active:
+            device.scan(d_img, spec.table, wl.bins, out, bin_range=brange, stream=stream)
+
+    for _ in range(args.warmup):
+        step(torch.cuda.Event(enable_timing=True))
+    barrier()
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
@@ -231,90 +294,121 @@ def run_ours(args, rank, world, local_rank):
         barrier()
         for k in range(args.steps):
             starts[k].record(stream)
-            ev_mid = mids[k]
-            step()
+            step(mids[k])
             ends[k].record(stream)
         barrier()
     total_ms = starts[0].elapsed_time(ends[-1])
     scan_ms = sum(mids[k].elapsed_time(ends[k]) for k in range(args.steps)) / args.steps
     prep_ms = sum(starts[k].elapsed_time(mids[k]) for k in range(args.steps)) / args.steps
 
-    # ---- parity spot check of the timed output (frame f0), outside the timed region
-    import zlib
+    # ---- parity spot check of the timed output, outside the timed region
+    gold = golden()
+    crc_ok = True
+    if active:
+        if wl.key == "hd64":
+            crc_ok = f"{zlib.crc32(out[0].cpu().numpy().tobytes()):08x}" == \
+                gold["1920x1080x32_frames"][f0]
+        else:
+            planes = gold[f"{wl.width}x{wl.height}x{wl.bins}"]["plane_crc"]
+            crc_ok = f"{zlib.crc32(out[0, 0].cpu().numpy().tobytes()):08x}" == planes[b0]
 
-    with open(os.path.join(ROOT, "tests", "golden", "configs.json")) as fh:
-        gold = json.load(fh)["1920x1080x32_frames"]
-    crc_ok = f"{zlib.crc32(out[0].cpu().numpy().tobytes()):08x}" == gold[f0]
+    # ---- optional gather of bin slabs onto rank 0 (not part of the metric)
+    gather_ms = None
+    if args.gather and wl.shard == "bins" and world > 1:
+        barrier()
+        g_start = time.perf_counter()
+        full = sharding.gather_slabs(out[0] if active else None, wl.bins, wl.height, wl.width,
+                                     rank, world)
+        barrier()
+        gather_ms = reduce_max([1000 * (time.perf_counter() - g_start)])[0]
+        del full
 
     # ---- e2e through the host-buffer API (pinned H2D + kernels + pinned D2H)
     e2e = None
-    if args.e2e_steps > 0:
-        pipe = pipeline.FramePipeline(nloc, HEIGHT, WIDTH, spec, chunk=args.chunk)
-        h_in = pipeline.pinned_empty((nloc, HEIGHT, WIDTH), dtype=torch.uint8)
-        h_in.copy_(torch.from_numpy(host_frames))
-        h_out = pipeline.pinned_empty((nloc, BINS, HEIGHT, WIDTH))
-        pipe.run(h_in, h_out)  # warm-up
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(args.e2e_steps):
-            pipe.run(h_in, h_out)
-        barrier()
-        e2e_s = reduce_max([time.perf_counter() - t0])[0]
-        e2e = {"value": FRAMES * args.e2e_steps / e2e_s, "unit": UNIT,
-               "h2d_bytes_per_step": int(pipe.h2d_bytes) * world,
-               "d2h_bytes_per_step": int(pipe.d2h_bytes) * world,
-               "steps": args.e2e_steps, "timer": "host perf_counter around synchronized steps"}
-        crc_ok = crc_ok and f"{zlib.crc32(h_out[0].numpy().tobytes()):08x}" == gold[f0]
-        # the e2e roofline: a plain pinned D2H copy of one output slice (PCIe bound)
-        probe = out[: min(nloc, 4)].view(torch.int32)
-        dst = h_out[: probe.shape[0]].view(torch.int32)
-        torch.cuda.synchronize(dev)
-        t1 = time.perf_counter()
-        for _ in range(3):
-            dst.copy_(probe, non_blocking=True)
-        torch.cuda.synchronize(dev)
-        d2h_gbs = 3 * probe.numel() * 4 / (time.perf_counter() - t1) / 1e9
-        e2e["d2h_copy_gbs"] = d2h_gbs
-        e2e["e2e_out_gbs"] = e2e["value"] * OUT_BYTES_PER_HIST / 1e9 / world
-        e2e["frac_of_d2h_copy"] = e2e["e2e_out_gbs"] / d2h_gbs
-        del h_out, h_in, pipe
+    if args.e2e_steps > 0 and active:
+        try:
+            e2e = run_e2e(args, wl, spec, host, nloc, (b0, b1), out, dev, barrier, reduce_max,
+                          world)
+            crc_ok = crc_ok and e2e.pop("_crc_ok")
+        except (RuntimeError, MemoryError) as exc:  # e.g. pinned allocation failure
+            e2e = {"value": None, "unit": UNIT, "error": repr(exc)[:200]}
 
     total_ms, scan_ms, prep_ms, bad = reduce_max([total_ms, scan_ms, prep_ms,
                                                   0.0 if crc_ok else 1.0])
     if rank != 0:
         return
-    value = FRAMES * args.steps / (total_ms / 1000.0)
+    value = wl.frames * args.steps / (total_ms / 1000.0)
     peak, peak_src = measured_peaks()
-    achieved = nloc * ALG_BYTES_PER_HIST / (scan_ms / 1000.0) / 1e9
-    traffic = committed_traffic()
+    alg_launch = nloc * (wl.width * wl.height + 256 + 4 * nb * wl.width * wl.height)
+    achieved = alg_launch / (scan_ms / 1000.0) / 1e9
+    traffic = committed_traffic(wl)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-        "config": config_block(world),
-        "output_gbs": value * OUT_BYTES_PER_HIST / 1e9,
-        "hbm_frac_step": value * ALG_BYTES_PER_HIST / 1e9 / peak / world,
+        "config": config_block(wl, world),
+        "output_gbs": value * wl.out_bytes / 1e9,
+        "hbm_frac_step": value * wl.alg_bytes / 1e9 / peak / world,
         "roofline": {"bound": "hbm", "kernel": "k2_scan", "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic * nloc if traffic else None),
-                     "alg_bytes_per_launch": nloc * ALG_BYTES_PER_HIST,
-                     "launch_ms": scan_ms, "prepare_ms": prep_ms},
-        "gpu_launches": launches_per_step * args.steps,
+                     "alg_bytes_per_launch": alg_launch, "launch_ms": scan_ms,
+                     "prepare_ms": prep_ms, "rank0_share": [f0, f1, b0, b1]},
+        "gpu_launches": plan["launches"] * args.steps,
         "plan": plan,
-        "parity": "frame 0 crc32 == reference golden" if not bad else "MISMATCH",
+        "parity": "rank-0 output crc32 == reference golden" if not bad else "MISMATCH",
         "clocks": clocks.summary(),
     }
+    if gather_ms is not None:
+        line["gather_ms"] = gather_ms
     if e2e is not None:
         line["e2e"] = e2e
-    if world == 1 and args.cpu_baseline_frames > 0:
-        from oracle import oracle as O
-
-        dt, n = cpu_reference_sample(range(args.cpu_baseline_frames))
-        line["cpu_baseline"] = {
-            "value": n / dt, "unit": UNIT, "cores": O.max_threads(), "kind": "port",
-            "sample": f"{n} HD frames (seeds 0..{n - 1}) through the C port of reference "
-                      f"compute_crossweave (strategies.py:129-150), all host threads"}
+    if world == 1 and args.cpu_baseline:
+        v, cores, sample = cpu_sample(wl, budget_s=args.ref_budget)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": sample}
     print(json.dumps(line), flush=True)
+
+
+def run_e2e(args, wl, spec, host, nloc, brange, out, dev, barrier, reduce_max, world):
+    """Host buffers in, host buffers out, through pipeline.FramePipeline."""
+    import torch
+
+    from paper_1711_01919_b200 import pipeline
+
+    b0, b1 = brange
+    pipe = pipeline.FramePipeline(nloc, wl.height, wl.width, spec, chunk=args.chunk,
+                                  bin_range=(b0, b1))
+    h_in = pipeline.pinned_empty((nloc, wl.height, wl.width), dtype=torch.uint8)
+    h_in.copy_(torch.from_numpy(host[:nloc]))
+    h_out = pipeline.pinned_empty((nloc, b1 - b0, wl.height, wl.width))
+    pipe.run(h_in, h_out)  # warm-up
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        pipe.run(h_in, h_out)
+    barrier()
+    e2e_s = reduce_max([time.perf_counter() - t0])[0]
+    res = {"value": wl.frames * args.e2e_steps / e2e_s, "unit": UNIT,
+           "h2d_bytes_per_step": int(pipe.h2d_bytes) * world,
+           "d2h_bytes_per_step": int(pipe.d2h_bytes) * world,
+           "steps": args.e2e_steps, "timer": "host perf_counter around synchronized steps"}
+    res["_crc_ok"] = bool(torch.equal(h_out[0, 0].view(torch.int32),
+                                      out[0, 0].view(torch.int32).cpu()))
+    # the e2e roofline: a plain pinned D2H copy of one output slice (PCIe bound)
+    probe = out[: min(nloc, 4)].view(torch.int32)
+    dst = h_out[: probe.shape[0]].view(torch.int32)
+    torch.cuda.synchronize(dev)
+    t1 = time.perf_counter()
+    for _ in range(3):
+        dst.copy_(probe, non_blocking=True)
+    torch.cuda.synchronize(dev)
+    d2h_gbs = 3 * probe.numel() * 4 / (time.perf_counter() - t1) / 1e9
+    res["d2h_copy_gbs"] = d2h_gbs
+    res["e2e_out_gbs_per_gpu"] = pipe.d2h_bytes * args.e2e_steps / e2e_s / 1e9
+    res["frac_of_d2h_copy"] = res["e2e_out_gbs_per_gpu"] / d2h_gbs
+    del h_out, h_in, pipe
+    return res
 
 
 def main():
@@ -323,18 +417,22 @@ def main():
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="hd64", choices=sorted(WORKLOADS))
+    ap.add_argument("--gather", action="store_true", help="time an NCCL gather of bin slabs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=4, help="frames per pipelined e2e chunk")
-    ap.add_argument("--cpu-baseline-frames", type=int, default=64)
-    ap.add_argument("--ref-frames", type=int, default=16, help="frames per reference-arm step")
+    ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--ref-budget", type=float, default=10.0,
+                    help="seconds of CPU work per reference sample (bounded)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
+    wl = WORKLOADS[args.workload]
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
-        run_reference(args, rank, world)
+        run_reference(args, wl, rank, world)
         return
     if world > 1:
         import torch
@@ -348,7 +446,7 @@ def main():
         else:
             dist.init_process_group(backend)
     try:
-        run_ours(args, rank, world, local_rank)
+        run_ours(args, wl, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

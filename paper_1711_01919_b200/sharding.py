@@ -62,6 +62,10 @@ def gather_slabs(slab: torch.Tensor | None, bins: int, height: int, width: int, 
     import torch.distributed as dist
 
     slabs = bin_slabs(bins, world)
+    # gloo cannot move CUDA tensors: stage through host memory (tests / 1-GPU runs)
+    staged = dist.get_backend(group) != "nccl" and slab is not None and slab.is_cuda
+    if staged:
+        slab = slab.cpu()
     if rank == root:
         dev = slab.device if slab is not None else torch.device("cpu")
         full = torch.empty((bins, height, width), dtype=torch.int32, device=dev)

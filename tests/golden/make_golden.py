@@ -72,6 +72,9 @@ def configs():
         ih = inthist.compute(img, inthist.BinSpec.uniform(b), inthist.CROSSWEAVE)
         res[f"{w}x{h}x{b}"] = {"seed": 0, "crc": tensor_checksum(ih),
                               "img_crc": f"{zlib.crc32(img.pixels.tobytes()):08x}"}
+        if (w, h) == (3840, 2160):  # per-plane crcs for bin-shard checks
+            res[f"{w}x{h}x{b}"]["plane_crc"] = [
+                f"{zlib.crc32(ih.counts[k].astype('<u4').tobytes()):08x}" for k in range(b)]
         print(w, h, b, res[f"{w}x{h}x{b}"], flush=True)
     spec = inthist.BinSpec.uniform(32)
     frames = []

@@ -100,7 +100,7 @@ def test_workspace_plan():
         n = L.ih_workspace_bytes(frames, 1080, 1920, 32, 0)
         assert n > 0 and n % (frames * 32 * 1920 * 2) == 0
     # tiny problems with few rows need no carries
-    assert L.ih_workspace_bytes(1, 40, 64, 4, 0) == 0
+    assert L.ih_workspace_bytes(1, 20, 64, 4, 0) == 0
     # cross-weave needs none; too-wide images fall back to cross-weave under auto
     assert L.ih_workspace_bytes(1, 1080, 1920, 32, _native.KERNEL_CROSSWEAVE) == 0
     assert L.ih_workspace_bytes(1, 16, 20000, 8, 0) == 0
