@@ -127,37 +127,48 @@ class ClockSampler:
         self.max_mhz = None
         self._stop = threading.Event()
 
-    def _run(self):
-        import pynvml as N
-
-        N.nvmlInit()
-        h = N.nvmlDeviceGetHandleByIndex(self.index)
-        self.max_mhz = N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM)
-        while not self._stop.is_set():
-            self.samples.append(N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM))
-            try:
-                bits = N.nvmlDeviceGetCurrentClocksEventReasons(h)
-            except AttributeError:
-                bits = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-            for name, bit in self.REASONS.items():
-                if bits & bit:
-                    self.reasons.add(name)
-            self._stop.wait(0.005)
-
-    def _safe_run(self):
+    def _sample(self):
+        N = self._nvml
+        self.samples.append(N.nvmlDeviceGetClockInfo(self._h, N.NVML_CLOCK_SM))
         try:
-            self._run()
-        except Exception as exc:  # NVML missing: report, do not fail the bench
+            bits = N.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+        except AttributeError:
+            bits = N.nvmlDeviceGetCurrentClocksThrottleReasons(self._h)
+        for name, bit in self.REASONS.items():
+            if bits & bit:
+                self.reasons.add(name)
+
+    def _loop(self):
+        try:
+            while not self._stop.wait(0.005):
+                self._sample()
+        except Exception as exc:
             self.error = repr(exc)
 
     def __enter__(self):
-        self.thread = threading.Thread(target=self._safe_run, daemon=True)
-        self.thread.start()
+        self._nvml = None
+        try:  # NVML initialised here, so the first sample is at the region's start
+            import pynvml as N
+
+            N.nvmlInit()
+            self._nvml = N
+            self._h = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = N.nvmlDeviceGetMaxClockInfo(self._h, N.NVML_CLOCK_SM)
+            self._sample()
+            self.thread = threading.Thread(target=self._loop, daemon=True)
+            self.thread.start()
+        except Exception as exc:  # NVML missing: report, do not fail the bench
+            self.error = repr(exc)
         return self
 
     def __exit__(self, *exc):
         self._stop.set()
-        self.thread.join(timeout=5)
+        if self._nvml is not None:
+            self.thread.join(timeout=5)
+            try:
+                self._sample()  # and one at its end
+            except Exception:
+                pass
 
     def summary(self):
         if not self.samples:
@@ -277,29 +288,58 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     plan = device.plan(nloc, wl.height, wl.width, nb,
                        aligned16=d_img.data_ptr() % 16 == 0) if active else {"launches": 0}
 
-    def step(ev_mid):
-        if active:
-            device.prepare(d_img, spec.table, wl.bins, bin_range=brange, stream=stream)
-        ev_mid.record(stream)
-        if active:
-            device.scan(d_img, spec.table, wl.bins, out, bin_range=brange, stream=stream)
+    # Steps are pipelined the way a video stream runs: the prepass of batch k+1
+    # (k2_colcounts: reads only the images) runs on a side stream into the
+    # other of two workspaces while batch k's scan (write-bound) runs.  Every
+    # step still executes both phases; --no-overlap serialises them.
+    side = torch.cuda.Stream(dev)
+    nws = max(1, device.workspace_bytes(max(nloc, 1), wl.height, wl.width, max(nb, 1)))
+    wss = [torch.empty(nws, dtype=torch.uint8, device=dev) for _ in range(2)]
 
-    for _ in range(args.warmup):
-        step(torch.cuda.Event(enable_timing=True))
+    def run_steps(n, ev_scan0=None, ev_scan1=None):
+        """Issue n steps; returns per-step (scan start, scan end) events."""
+        before = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        after = [torch.cuda.Event(enable_timing=True) for _ in range(n)]
+        prep_done = [torch.cuda.Event() for _ in range(n)]
+
+        def issue_prep(k):
+            s_prep = side if args.overlap else stream
+            if args.overlap:
+                s_prep.wait_event(kick)
+                if k >= 2:
+                    s_prep.wait_event(after[k - 2])  # workspace k % 2 is free again
+            if active:
+                device.prepare(d_img, spec.table, wl.bins, bin_range=brange, stream=s_prep,
+                               workspace=wss[k % 2])
+            prep_done[k].record(s_prep)
+
+        kick = torch.cuda.Event()
+        kick.record(stream)
+        issue_prep(0)
+        for k in range(n):
+            stream.wait_event(prep_done[k])
+            before[k].record(stream)
+            if active:
+                device.scan(d_img, spec.table, wl.bins, out, bin_range=brange, stream=stream,
+                            workspace=wss[k % 2])
+            after[k].record(stream)
+            if k + 1 < n:
+                issue_prep(k + 1)
+        return before, after
+
+    run_steps(args.warmup)
     barrier()
-    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    mids = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     with ClockSampler(dev_index) as clocks:
         barrier()
-        for k in range(args.steps):
-            starts[k].record(stream)
-            step(mids[k])
-            ends[k].record(stream)
+        t_start = torch.cuda.Event(enable_timing=True)
+        t_end = torch.cuda.Event(enable_timing=True)
+        t_start.record(stream)
+        befores, afters = run_steps(args.steps)
+        t_end.record(stream)
         barrier()
-    total_ms = starts[0].elapsed_time(ends[-1])
-    scan_ms = sum(mids[k].elapsed_time(ends[k]) for k in range(args.steps)) / args.steps
-    prep_ms = sum(starts[k].elapsed_time(mids[k]) for k in range(args.steps)) / args.steps
+    total_ms = t_start.elapsed_time(t_end)
+    scan_ms = sum(b.elapsed_time(a) for b, a in zip(befores, afters)) / args.steps
+    prep_ms = max(0.0, total_ms / args.steps - scan_ms)  # exposed (not overlapped) part
 
     # ---- parity spot check of the timed output, outside the timed region
     gold = golden()
@@ -353,7 +393,8 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
                      "traffic": (traffic * nloc if traffic else None),
                      "alg_bytes_per_launch": alg_launch, "launch_ms": scan_ms,
-                     "prepare_ms": prep_ms, "rank0_share": [f0, f1, b0, b1]},
+                     "prepare_exposed_ms": prep_ms, "rank0_share": [f0, f1, b0, b1]},
+        "pipelined_steps": bool(args.overlap),
         "gpu_launches": plan["launches"] * args.steps,
         "plan": plan,
         "parity": "rank-0 output crc32 == reference golden" if not bad else "MISMATCH",
@@ -422,6 +463,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=4, help="frames per pipelined e2e chunk")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-overlap", dest="overlap", action="store_false",
+                    help="run each step's prepass and scan back to back on one stream")
     ap.add_argument("--ref-budget", type=float, default=10.0,
                     help="seconds of CPU work per reference sample (bounded)")
     args = ap.parse_args()

@@ -294,12 +294,19 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
   const int nslab = (p.nbp + ih::kCountSlab - 1) / ih::kCountSlab;
   dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)(c.frames * nslab));
   const bool al = aligned_rows(c);
-  auto kern = al ? ih::k2_colcounts<true> : ih::k2_colcounts<false>;
-  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)ih::kCountSmem) != cudaSuccess)
+  // warps per colcounts CTA: ~48+ rows per warp, 2..8 warps
+  const int nw = p.S >= 384 ? 8 : p.S >= 192 ? 4 : 2;
+  auto kern = al ? (nw == 8 ? ih::k2_colcounts<true, 8>
+                            : nw == 4 ? ih::k2_colcounts<true, 4> : ih::k2_colcounts<true, 2>)
+                 : (nw == 8 ? ih::k2_colcounts<false, 8>
+                            : nw == 4 ? ih::k2_colcounts<false, 4> : ih::k2_colcounts<false, 2>);
+  const size_t smem = nw * ih::kCountWarpSmem;
+  if (smem > 48 * 1024 &&
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess)
     return cuda_fail("k2_colcounts smem attribute");
-  kern<<<grid, ih::kCountWarps * 32, ih::kCountSmem, c.stream>>>(
-      c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S, p.nseg, p.nbp, p.Wp, nslab, (uint16_t*)ws);
+  kern<<<grid, nw * 32, smem, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S, p.nseg,
+                                          p.nbp, p.Wp, nslab, (uint16_t*)ws);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts");
   if (!table_prefix_h(p, c.H)) return IH_OK;  // the scan kernel sums the count slots
   const int64_t total = c.frames * p.nbp * p.Wp / 4;

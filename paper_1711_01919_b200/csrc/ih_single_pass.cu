@@ -37,11 +37,13 @@ namespace ih {
 // < 65536 (host-enforced).  Pixels past the right edge map to LUT entry 256+.
 // ---------------------------------------------------------------------------
 constexpr int kCountSlab = 32;
-constexpr int kCountWarps = 8;
 constexpr int kCountRows = kCountSlab + 1;  // + a dummy row for "no bin in this slab"
-constexpr size_t kCountSmem = (size_t)kCountWarps * kCountRows * 4 * 32 * sizeof(uint16_t);
+// shared bytes of one warp's private histogram
+constexpr size_t kCountWarpSmem = (size_t)kCountRows * 4 * 32 * sizeof(uint16_t);
 
-template <bool ALIGNED>
+// NW warps per CTA (2, 4 or 8): fewer for short segments, where zeroing and
+// summing the private histograms would otherwise dominate
+template <bool ALIGNED, int kCountWarps>
 __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
     RelLut lut, int S, int nseg, int nbp, int64_t Wp, int nslab, uint16_t* __restrict__ ws) {
@@ -61,7 +63,8 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
   }
   {
     uint4* z = reinterpret_cast<uint4*>(chist);
-    for (int i = threadIdx.x; i < (int)(kCountSmem / 16); i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < (int)(kCountWarps * kCountWarpSmem / 16); i += blockDim.x)
+      z[i] = make_uint4(0, 0, 0, 0);
   }
   uint32_t inval[4];
 #pragma unroll

@@ -40,7 +40,7 @@ def _stream_handle(dev: torch.device, stream=None) -> int:
     return int(s.cuda_stream)
 
 
-def workspace(dev: torch.device, nbytes: int) -> torch.Tensor:
+def workspace_(dev: torch.device, nbytes: int) -> torch.Tensor:
     """Per-device scratch buffer, grown on demand (caller-owned per the ABI)."""
     idx = dev.index
     ws = _workspaces.get(idx)
@@ -120,13 +120,15 @@ def empty_output(frames: int, slab_bins: int, height: int, width: int, device) -
 
 
 def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, out=None,
-                       kernel: str = "auto", stream=None) -> torch.Tensor:
+                       kernel: str = "auto", stream=None, workspace=None) -> torch.Tensor:
     """Integral histograms of (F, H, W) or (H, W) uint8 CUDA frames.
 
     Returns (F, hi-lo, H, W) torch.uint32 (or (hi-lo, H, W) for a 2D input):
     the bin-major tensor of IntegralHistogram.counts (core.py:106-116) for the
     bins [lo, hi) of ``bin_range`` (default: all).  Bit-identical to every
-    reference strategy (strategies.py:109-229).
+    reference strategy (strategies.py:109-229).  The default scratch buffer is
+    per device: concurrent calls on different streams pass their own
+    ``workspace`` (a uint8 CUDA tensor of ``workspace_bytes(...)`` bytes).
     """
     squeeze = images.dim() == 2 and out is None
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
@@ -140,35 +142,49 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
             raise ShapeError("out must be a contiguous uint32 tensor")
         if out.numel() != a.frames * nb * a.H * a.W or out.device != a.dev:
             raise ShapeError("out has the wrong size or device")
-    ws_n = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, nb, a.kernel)
-    ws = workspace(a.dev, ws_n)
+    ws = _workspace_for(a, workspace)
     L = _native.lib()
     _native.check(L.ih_integral_histogram(
         a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
-        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel(), a.kernel, a.stream))
+        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
+        a.kernel, a.stream))
     if squeeze and out.dim() == 4:
         return out[0]
     return out
 
 
-def prepare(images, table, bins, bin_range=None, kernel="auto", stream=None) -> None:
-    """Phase 1 of integral_histogram (segment carries), for per-kernel timing."""
+def _workspace_for(a: "_Args", workspace) -> torch.Tensor:
+    need = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, a.hi - a.lo, a.kernel)
+    if workspace is None:
+        return workspace_(a.dev, need)
+    if workspace.numel() * workspace.element_size() < need or not workspace.is_cuda:
+        raise ParameterError(f"workspace needs {need} bytes on the device")
+    return workspace
+
+
+def prepare(images, table, bins, bin_range=None, kernel="auto", stream=None,
+            workspace=None) -> None:
+    """Phase 1 of integral_histogram (row-segment carries into the workspace).
+
+    Reads only the images: with a caller-owned ``workspace`` per in-flight
+    batch, the phase for batch k+1 can run on a side stream while batch k's
+    scan (write-bound) runs."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
-    ws_n = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, a.hi - a.lo, a.kernel)
-    ws = workspace(a.dev, ws_n)
+    ws = _workspace_for(a, workspace)
     _native.check(_native.lib().ih_ih_prepare(
         a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
-        a.bins, a.lo, a.hi, ws.data_ptr(), ws.numel(), a.kernel, a.stream))
+        a.bins, a.lo, a.hi, ws.data_ptr(), ws.numel() * ws.element_size(), a.kernel, a.stream))
 
 
-def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None) -> torch.Tensor:
+def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None,
+         workspace=None) -> torch.Tensor:
     """Phase 2 of integral_histogram (the dominant single-pass kernel)."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
-    ws_n = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, a.hi - a.lo, a.kernel)
-    ws = workspace(a.dev, ws_n)
+    ws = _workspace_for(a, workspace)
     _native.check(_native.lib().ih_ih_scan(
         a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
-        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel(), a.kernel, a.stream))
+        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
+        a.kernel, a.stream))
     return out
 
 
