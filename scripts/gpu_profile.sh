@@ -8,9 +8,9 @@ timeout 600 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_${TAG}.json
 echo bench=$?
 timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
   --log-file gpurun_out/launches_${TAG}.csv \
-  python bench.py --steps 10 --warmup 3 --e2e-steps 0 --cpu-baseline-frames 0 > /dev/null 2>&1
+  python bench.py --steps 10 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 echo ncu_launches=$?
 timeout 400 ncu --set full --clock-control none --import-source on -k regex:k2_scan -s 3 -c 1 \
   -o gpurun_out/prof_k2_${TAG} -f \
-  python bench.py --steps 1 --warmup 3 --e2e-steps 0 --cpu-baseline-frames 0 > /dev/null 2>&1
+  python bench.py --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 echo ncu_full=$?
