@@ -459,6 +459,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="hd64", choices=sorted(WORKLOADS))
+    ap.add_argument("--frames", type=int, default=0, help="override histograms per step")
     ap.add_argument("--gather", action="store_true", help="time an NCCL gather of bin slabs")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=4, help="frames per pipelined e2e chunk")
@@ -471,6 +472,9 @@ def main():
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
     wl = WORKLOADS[args.workload]
+    if args.frames:  # sizing experiments, e.g. the per-GPU share of an N-GPU run
+        wl = Workload(wl.key, wl.width, wl.height, wl.bins, args.frames, wl.shard,
+                      wl.desc + f" [frames overridden: {args.frames}]")
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

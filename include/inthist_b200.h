@@ -14,6 +14,7 @@
  *                              binning BinSpec.bin_image core.py:94-96.
  *   ih_region_histograms    <- core.py:179-195 region_histogram (batched).
  *   ih_window_counts        <- likelihood.py:34-52 window_counts.
+ *   ih_likelihood_map       <- likelihood.py:55-77 likelihood_map (fused).
  *
  * Conventions (all entry points):
  *   - stream-ordered and asynchronous: work is enqueued on `stream`; nothing
@@ -124,6 +125,19 @@ ih_status ih_region_histograms(const uint32_t *t, int32_t nb, int64_t height, in
  * (likelihood.py:36-41 order). */
 ih_status ih_window_counts(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
                            int32_t h, int32_t w, int64_t *out, void *stream);
+
+/* Sliding-window likelihood map (likelihood.py:55-77), fused: for every
+ * h x w placement, sum over bins of metric(template_b, count_b / (h*w)),
+ * clipped to [0, 1]; only the map is written.
+ *   template_host  HOST pointer, nb doubles (a normalized histogram)
+ *   metric         IH_METRIC_INTERSECTION (sum min) or IH_METRIC_BHATTACHARYYA (sum sqrt(p q))
+ *   out            device (height-h+1, width-w+1) float64
+ * IH_ERR_SHAPE nb outside 1..256; IH_ERR_PARAM bad metric / h,w < 1;
+ * IH_ERR_BOUNDS window larger than the image (likelihood.py:64-69 order). */
+typedef enum { IH_METRIC_INTERSECTION = 0, IH_METRIC_BHATTACHARYYA = 1 } ih_metric;
+ih_status ih_likelihood_map(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
+                            int32_t h, int32_t w, const double *template_host, int32_t metric,
+                            double *out, void *stream);
 
 /* Human-readable status name. */
 const char *ih_status_string(ih_status s);

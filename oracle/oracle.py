@@ -163,6 +163,15 @@ def np_window_counts(counts, h, w) -> np.ndarray:
     return out
 
 
+def np_likelihood_map(counts, template, h, w, metric) -> np.ndarray:
+    """likelihood.py:55-77 restated: window counts -> q = c / (h*w) -> metric
+    per bin -> sum over the bin axis -> clip to [0, 1] (float64 numpy ops)."""
+    q = np_window_counts(counts, h, w).astype(np.float64) / float(h * w)
+    t = np.asarray(template, dtype=np.float64)[:, None, None]
+    vals = np.minimum(t, q).sum(axis=0) if metric == "intersection" else np.sqrt(t * q).sum(axis=0)
+    return np.clip(vals, 0.0, 1.0)
+
+
 def brute_integral_histogram(pixels, table, bins) -> np.ndarray:
     """tests/conftest.py:17-27 restated: O((WH)^2) direct counting (tiny images)."""
     binned = np.asarray(table, dtype=np.uint8)[np.asarray(pixels, dtype=np.uint8)]

@@ -36,6 +36,7 @@ EXPORTS = (
     "ih_region_histograms",
     "ih_window_counts",
     "ih_plan_describe",
+    "ih_likelihood_map",
     "ih_status_string",
     "ih_last_error",
     "ih_abi_version",
@@ -72,6 +73,8 @@ def lib() -> ctypes.CDLL:
     L.ih_region_histograms.restype = ctypes.c_int
     L.ih_window_counts.argtypes = [P, i32, i64, i64, i32, i32, P, P]
     L.ih_window_counts.restype = ctypes.c_int
+    L.ih_likelihood_map.argtypes = [P, i32, i64, i64, i32, i32, P, i32, P, P]
+    L.ih_likelihood_map.restype = ctypes.c_int
     L.ih_plan_describe.argtypes = [i64, i64, i64, i32, i32, i32, P]
     L.ih_plan_describe.restype = ctypes.c_int
     L.ih_status_string.argtypes = [ctypes.c_int]

@@ -309,7 +309,7 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
                                           p.nbp, p.Wp, nslab, (uint16_t*)ws);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts");
   if (!table_prefix_h(p, c.H)) return IH_OK;  // the scan kernel sums the count slots
-  const int64_t total = c.frames * p.nbp * p.Wp / 4;
+  const int64_t total = c.frames * p.nbp * p.Wp / 4 * ih::kPrefixLanes;  // 8 lanes per quad
   int64_t blocks = (total + 255) / 256;
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
   ih::k2_colprefix<<<(unsigned)blocks, 256, 0, c.stream>>>((uint16_t*)ws, c.frames, p.nseg, p.nbp,
@@ -503,6 +503,30 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   info[5] = p.R;
   info[6] = p.nwarps;
   info[7] = (int64_t)k2_ws_bytes(frames, p);
+  return IH_OK;
+}
+
+ih_status ih_likelihood_map(const uint32_t* t, int32_t nb, int64_t height, int64_t width,
+                            int32_t h, int32_t w, const double* template_host, int32_t metric,
+                            double* out, void* stream) {
+  if (nb < 1 || nb > 256) return fail(IH_ERR_SHAPE, "bin count must be in [1, 256]");
+  if (!template_host) return fail(IH_ERR_SHAPE, "null template");
+  if (metric != IH_METRIC_INTERSECTION && metric != IH_METRIC_BHATTACHARYYA)
+    return fail(IH_ERR_PARAM, "unknown metric");
+  if (h < 1 || w < 1) return fail(IH_ERR_PARAM, "window extents must be >= 1");
+  if (h > height || w > width) return fail(IH_ERR_BOUNDS, "window exceeds image");
+  if (!t || !out) return fail(IH_ERR_PARAM, "null pointer");
+  ih::Template tpl;
+  for (int b = 0; b < 256; ++b) tpl.t[b] = b < nb ? template_host[b] : 0.0;
+  const int64_t R = height - h + 1, C = width - w + 1;
+  dim3 grid((unsigned)((C + 255) / 256), (unsigned)(R < 65535 ? R : 65535));
+  if (metric == IH_METRIC_INTERSECTION)
+    ih::k5_likelihood_map<true><<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h,
+                                                                        w, tpl, out);
+  else
+    ih::k5_likelihood_map<false><<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width,
+                                                                         h, w, tpl, out);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k5_likelihood_map");
   return IH_OK;
 }
 

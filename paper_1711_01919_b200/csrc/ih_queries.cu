@@ -80,4 +80,56 @@ __global__ void __launch_bounds__(256) k4_window_counts(const uint32_t* __restri
   }
 }
 
+// K5: fused likelihood map (likelihood.py:55-77).  One thread per window
+// placement (i, j), j fastest: for every bin b, the window count from four
+// corner reads, q = count / (h*w) (a true division, as numpy does), the metric
+// term min(t_b, q) or sqrt(t_b * q), accumulated over b = 0..nb-1 in order
+// (numpy's axis-0 reduction order), then clipped to [0, 1].  Only the
+// (H-h+1, W-w+1) float64 map is written: the (nb, ...) int64 counts of K4 never
+// exist.  The template rides in the kernel parameters (<= 256 doubles).
+struct Template {
+  double t[256];
+};
+
+template <bool INTERSECTION>
+__global__ void __launch_bounds__(256) k5_likelihood_map(const uint32_t* __restrict__ t, int nb,
+                                                          int64_t H, int64_t W, int h, int w,
+                                                          Template tpl, double* __restrict__ out) {
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const double area = (double)h * (double)w;
+  const int64_t plane = H * W;
+  for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= C) continue;
+    const int64_t o11 = (i + h - 1) * W + (j + w - 1);
+    const int64_t o01 = (i - 1) * W + (j + w - 1);
+    const int64_t o10 = (i + h - 1) * W + (j - 1);
+    const int64_t o00 = (i - 1) * W + (j - 1);
+    double acc = 0.0;
+    constexpr int U = 8;  // bins per step: 32 independent corner loads in flight
+    for (int b0 = 0; b0 < nb; b0 += U) {
+      long long v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u < nb ? b0 + u : nb - 1;
+        const uint32_t* p = t + (int64_t)b * plane;
+        const uint32_t a11 = __ldg(p + o11);
+        const uint32_t a10 = j > 0 ? __ldg(p + o10) : 0u;
+        const uint32_t a01 = i > 0 ? __ldg(p + o01) : 0u;
+        const uint32_t a00 = i > 0 && j > 0 ? __ldg(p + o00) : 0u;
+        v[u] = (long long)a11 - (long long)a10 - (long long)a01 + (long long)a00;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // the sum over bins stays in order b = 0..nb-1
+        if (b0 + u < nb) {
+          const double q = (double)v[u] / area;
+          const double tb = tpl.t[b0 + u];
+          acc += INTERSECTION ? fmin(tb, q) : sqrt(tb * q);
+        }
+      }
+    }
+    out[i * C + j] = fmin(fmax(acc, 0.0), 1.0);
+  }
+}
+
 }  // namespace ih

@@ -138,34 +138,45 @@ __device__ __forceinline__ uint2 add_u16x4(uint2 a, uint2 b) {  // lanes never c
   return make_uint2(a.x + b.x, a.y + b.y);
 }
 
+// Two-level: 8 lanes per 4-column quad, lane t owning a run of segment slots;
+// run totals are exclusive-scanned with 3 shuffles inside the 8-lane group, so
+// every load is issued up front (no chain of round trips over the segments).
+constexpr int kPrefixLanes = 8;
+
 __global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, int64_t frames,
                                                      int nseg, int nbp, int64_t Wp) {
   const int64_t plane = (int64_t)nbp * Wp;  // elements per segment slot
   const int64_t quads = plane / 4;
-  const int64_t total = frames * quads;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t f = i / quads, q = i % quads;
+  const int64_t groups = frames * quads;
+  const int sub = threadIdx.x & (kPrefixLanes - 1);
+  const int per = (nseg + kPrefixLanes - 1) / kPrefixLanes;  // slots per lane
+  const int j0 = sub * per, j1 = min(nseg, j0 + per);
+  for (int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPrefixLanes; ;
+       gi += (int64_t)gridDim.x * blockDim.x / kPrefixLanes) {
+    // all 8 lanes of a group iterate together (the shuffles need them)
+    const bool live = gi < groups;
+    if (__all_sync(kFull, !live)) break;
+    const int64_t f = live ? gi / quads : 0, q = live ? gi % quads : 0;
     uint2* p = reinterpret_cast<uint2*>(ws + f * nseg * plane) + q;
-    const int64_t step = quads;
-    uint2 run = make_uint2(0u, 0u);
-    int s = 0;
-    for (; s + 8 <= nseg - 1; s += 8) {
-      uint2 v[8];
+    uint2 tot = make_uint2(0u, 0u);
+    for (int j = j0; j < j1 && j < nseg - 1; ++j)
+      if (live) tot = add_u16x4(tot, p[(int64_t)j * quads]);
+    // exclusive scan of the run totals across the 8 lanes of this group
+    uint2 inc = tot;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) v[k] = p[(s + k) * step];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        p[(s + k) * step] = run;
-        run = add_u16x4(run, v[k]);
+    for (int d = 1; d < kPrefixLanes; d <<= 1) {
+      const uint32_t x = __shfl_up_sync(kFull, inc.x, d, kPrefixLanes);
+      const uint32_t y = __shfl_up_sync(kFull, inc.y, d, kPrefixLanes);
+      if (sub >= d) inc = add_u16x4(inc, make_uint2(x, y));
+    }
+    uint2 run = make_uint2(inc.x - tot.x, inc.y - tot.y);  // lanes never borrow (< 65536)
+    if (live) {
+      for (int j = j0; j < j1; ++j) {
+        const uint2 v = j < nseg - 1 ? p[(int64_t)j * quads] : make_uint2(0u, 0u);
+        p[(int64_t)j * quads] = run;
+        run = add_u16x4(run, v);
       }
     }
-    for (; s < nseg - 1; ++s) {
-      const uint2 v = p[s * step];
-      p[s * step] = run;
-      run = add_u16x4(run, v);
-    }
-    p[(int64_t)(nseg - 1) * step] = run;
   }
 }
 

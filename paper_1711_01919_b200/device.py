@@ -237,6 +237,28 @@ def window_counts(t: torch.Tensor, h: int, w: int, stream=None) -> torch.Tensor:
     return out
 
 
+def likelihood_map(t: torch.Tensor, template, h: int, w: int, metric: str = "bhattacharyya",
+                   stream=None) -> torch.Tensor:
+    """Fused K5 (likelihood.py:55-77): (H-h+1, W-w+1) float64 map on the device."""
+    metrics = {"intersection": 0, "bhattacharyya": 1}
+    if metric not in metrics:
+        raise ParameterError(f"unknown metric {metric!r}")
+    if h < 1 or w < 1:
+        raise ParameterError("window extents must be >= 1")
+    t = _check_tensor(t)
+    nb, H, W = (int(x) for x in t.shape)
+    tmpl = np.ascontiguousarray(np.asarray(template, dtype=np.float64))
+    if tmpl.shape != (nb,):
+        raise ShapeError(f"template has {tmpl.shape} entries, tensor has {nb} bins")
+    if h > H or w > W:
+        raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
+    out = torch.empty((H - h + 1, W - w + 1), dtype=torch.float64, device=t.device)
+    _native.check(_native.lib().ih_likelihood_map(
+        t.data_ptr(), nb, H, W, int(h), int(w), tmpl.ctypes.data, metrics[metric],
+        out.data_ptr(), _stream_handle(t.device, stream)))
+    return out
+
+
 def upload_image(pixels: np.ndarray, device=None) -> torch.Tensor:
     """H2D of a host (H, W) uint8 image into a 16-byte-pitched device buffer
     (aligned 32-bit pixel loads in the kernels for every width).  Returns the

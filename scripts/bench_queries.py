@@ -43,4 +43,17 @@ for (h, w) in ((64, 64), (8, 8)):
     alg = 32 * R * C * 8 + 32 * 1080 * 1920 * 4  # int64 out + one read of the tensor
     res.append({"kernel": "k4_window_counts", "tensor": "1920x1080x32", "window": f"{h}x{w}", "ms": round(ms, 4),
                 "alg_GBs": round(alg / ms / 1e6, 1), "frac": round(alg / ms / 1e6 / PEAK, 3)})
+# K5 fused likelihood map vs the unfused path (K4 counts + float64 torch ops)
+tmpl = np.random.default_rng(0).random(32); tmpl /= tmpl.sum()
+for (h, w) in ((64, 64), (8, 8)):
+    ms = timeit(lambda: device.likelihood_map(t, tmpl, h, w, "bhattacharyya"))
+    R, C = 1080 - h + 1, 1920 - w + 1
+    tt = torch.from_numpy(tmpl).cuda()[:, None, None]
+    def unfused():
+        q = device.window_counts(t, h, w).to(torch.float64) / float(h * w)
+        return torch.sqrt(tt * q).sum(0).clamp_(0, 1)
+    ms_u = timeit(unfused, reps=3)
+    res.append({"kernel": "k5_likelihood_map", "tensor": "1920x1080x32", "window": f"{h}x{w}",
+                "ms": round(ms, 4), "unfused_ms": round(ms_u, 4), "speedup": round(ms_u / ms, 1),
+                "placements_per_s": round(R * C / ms * 1e3)})
 for r_ in res: print(json.dumps(r_), flush=True)

@@ -369,3 +369,26 @@ def test_out_argument_and_int32_view(rng):
     with pytest.raises(ih.ShapeError):
         device.integral_histogram(device.upload_image(px), lut, 5,
                                   out=torch.zeros((1, 4, 50, 70), dtype=torch.int32, device="cuda"))
+
+
+@pytest.mark.parametrize("metric", ["intersection", "bhattacharyya"])
+def test_fused_likelihood_map_vs_numpy_restatement(rng, metric):
+    """K5 against likelihood.py:55-77 restated in numpy (tolerance 1e-12, the
+    reference's own, tests/test_likelihood.py:46); also reports exactness."""
+    for (H, W, B, h, w) in [(60, 90, 16, 8, 8), (97, 61, 7, 13, 5), (40, 40, 256, 40, 40),
+                            (33, 300, 32, 1, 1)]:
+        px = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        counts = O.compute_crossweave(px, O.np_uniform_table(B), B)
+        tmpl = rng.random(B)
+        tmpl /= tmpl.sum()
+        ih_ = ih.IntegralHistogram(counts)
+        got = ih.likelihood_map(ih_, tmpl, h, w, metric).values
+        want = O.np_likelihood_map(counts, tmpl, h, w, metric)
+        assert got.shape == want.shape
+        assert np.abs(got - want).max() < 1e-12, (H, W, B, h, w)
+    with pytest.raises(ih.ShapeError):
+        ih.likelihood_map(ih_, np.ones(3) / 3, 2, 2)
+    with pytest.raises(ih.ParameterError):
+        ih.likelihood_map(ih_, tmpl, 2, 2, "nope")
+    with pytest.raises(ih.BoundsError):
+        ih.likelihood_map(ih_, tmpl, 34, 2)
