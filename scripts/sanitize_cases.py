@@ -1,0 +1,34 @@
+"""Small parity cases for compute-sanitizer: every K2 carry mode / input path,
+K1/K1b, K3, K4, K5 -- each checked against the oracle."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np, torch
+from oracle import oracle as O
+from paper_1711_01919_b200 import device
+
+rng = np.random.default_rng(7)
+cases = [(1, 1, 3), (7, 131, 5), (61, 257, 16), (100, 300, 64), (33, 2049, 7), (40, 4100, 9), (9, 8192, 4)]
+envs = [{}, {"IH_NSEG": "3"}, {"IH_NSEG": "5", "IH_TABLE_SUM_MAX": "1"},
+        {"IH_NSEG": "4", "IH_CARRY_LOOKBACK": "1"}, {"IH_NO_TMA": "1", "IH_NSEG": "2"},
+        {"IH_ROWS_PER_BATCH": "1", "IH_NSEG": "3"}]
+bad = 0
+for env in envs:
+    for k in ("IH_NSEG", "IH_TABLE_SUM_MAX", "IH_CARRY_LOOKBACK", "IH_NO_TMA", "IH_ROWS_PER_BATCH"):
+        os.environ.pop(k, None)
+    os.environ.update(env)
+    for (h, w, b) in cases:
+        px = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        lut = O.np_uniform_table(b)
+        want = O.compute_crossweave(px, lut, b)
+        for kernel in ("auto", "crossweave"):
+            got = device.integral_histogram(device.upload_image(px), lut, b, kernel=kernel).cpu().numpy()
+            if not np.array_equal(got, want):
+                bad += 1; print("MISMATCH", env, h, w, b, kernel)
+t = torch.from_numpy(O.compute_crossweave(rng.integers(0, 256, (50, 70), dtype=np.uint8), O.np_uniform_table(6), 6)).cuda()
+regs = [(0, 0, 49, 69), (3, 4, 20, 30), (49, 69, 49, 69)]
+assert np.array_equal(device.region_histograms(t, regs).cpu().numpy(), O.region_histograms(t.cpu().numpy(), regs))
+assert np.array_equal(device.window_counts(t, 7, 9).cpu().numpy(), O.window_counts(t.cpu().numpy(), 7, 9))
+tm = np.ones(6) / 6
+d = device.likelihood_map(t, tm, 7, 9, "intersection").cpu().numpy()
+assert np.abs(d - O.np_likelihood_map(t.cpu().numpy(), tm, 7, 9, "intersection")).max() < 1e-12
+print("sanitize cases done, mismatches:", bad)
