@@ -200,29 +200,28 @@ int resolve_kernel(int kernel, const K2Plan& p) {
   return kernel;
 }
 
-// CARRY_TABLE with few segments skips k2_colprefix: the scan CTA of segment s
-// sums the s count slots above it (fewer bytes than a prefix pass for s <= 8).
+// CARRY_TABLE with up to 24 segments skips k2_colprefix: the scan CTA of
+// segment s sums the s count slots above it (L2-resident, 4 slots in flight).
 // u16 prefixes need H <= 65535; taller images always sum counts in the scan.
 bool table_prefix_h(const K2Plan& p, int64_t H) {
   return H <= 65535 && p.nseg > env_int("IH_TABLE_SUM_MAX", 24);
 }
 
 // Workspace layouts.
-//   CARRY_TABLE:    (frames, nseg, nbp, Wp) u32 column-prefix table.
+//   CARRY_TABLE:    (frames, nseg, nbp, Wp) u16 column counts (or prefixes).
 //   CARRY_LOOKBACK: [ticket | pad 16 B][flags: ntiles u32, 16 B padded]
 //                   [agg: ntiles x 4 x Wp u32][incl: ntiles x 4 x Wp u32]
 int64_t lb_tiles(int64_t frames, const K2Plan& p) { return frames * p.ngroups * p.nseg; }
 size_t lb_header_bytes(int64_t frames, const K2Plan& p) {
   return 16 + (size_t)((lb_tiles(frames, p) * 4 + 15) / 16 * 16);
 }
-size_t k2_ws_bytes_plan(int64_t frames, const K2Plan& p) {
+size_t k2_ws_bytes(int64_t frames, const K2Plan& p) {
   if (p.carry == ih::CARRY_TABLE) return (size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint16_t);
   if (p.carry == ih::CARRY_LOOKBACK)
     return lb_header_bytes(frames, p) +
            2 * (size_t)lb_tiles(frames, p) * ih::kGroup * p.Wp * sizeof(uint32_t);
   return 0;
 }
-size_t k2_ws_bytes(int64_t frames, const K2Plan& p) { return k2_ws_bytes_plan(frames, p); }
 
 struct Call {
   const uint8_t* img;
