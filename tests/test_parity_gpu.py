@@ -392,3 +392,23 @@ def test_fused_likelihood_map_vs_numpy_restatement(rng, metric):
         ih.likelihood_map(ih_, tmpl, 2, 2, "nope")
     with pytest.raises(ih.BoundsError):
         ih.likelihood_map(ih_, tmpl, 34, 2)
+
+
+@pytest.mark.parametrize("piece_bytes", [1 << 30, 3 * 60 * 90 * 4])
+def test_frame_pipeline_host_to_host(rng, piece_bytes):
+    """pipeline.FramePipeline: pinned H2D, kernels, pinned D2H through a two-slot
+    ring, in frame chunks or (small pieces) bin sub-slabs of single frames."""
+    from paper_1711_01919_b200 import pipeline
+
+    frames = rng.integers(0, 256, (5, 60, 90), dtype=np.uint8)
+    spec = ih.BinSpec.uniform(11)
+    pipe = pipeline.FramePipeline(5, 60, 90, spec, chunk=2, bin_range=(2, 9),
+                                  max_piece_bytes=piece_bytes)
+    h_in = pipeline.pinned_empty((5, 60, 90), dtype=torch.uint8)
+    h_in.copy_(torch.from_numpy(frames))
+    h_out = pipeline.pinned_empty((5, 7, 60, 90))
+    for _ in range(2):
+        pipe.run(h_in, h_out)
+        for f in range(5):
+            want = O.compute_crossweave(frames[f], spec.table, 11)[2:9]
+            assert np.array_equal(h_out[f].numpy(), want)
