@@ -309,11 +309,25 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
   const int nb_count = count_pass ? nbatch : 0;
   const int nb_total = nb_count + nbatch;
 
-  build_onehot(oh, lut, g);
+  // ring batch b -> first row (pass 0 = counting, pass 1 = scan)
+  auto batch_row0 = [&](int b) { return rs + (int64_t)(b < nb_count ? b : b - nb_count) * R; };
+  auto issue = [&](int b) {  // producer: thread 0 only
+    const int stage = b % NST;
+    const int64_t r0 = batch_row0(b);
+    const int rows = (int)(re - r0 < R ? re - r0 : R);
+    mbar_expect_tx(&full_bar[stage], (uint32_t)rows * a.row_bytes);
+    for (int rr = 0; rr < rows; ++rr)
+      tma_row(ring + ((size_t)stage * R + rr) * a.Wp, img + (r0 + rr) * a.pitch, a.row_bytes,
+              &full_bar[stage]);
+  };
+  // start the image stream first: the ring fill overlaps the table build below
+  // (nobody waits on a barrier before the __syncthreads that follows)
   if (TMA && threadIdx.x == 0) {
     for (int i = 0; i < NST; ++i) mbar_init(&full_bar[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int b = 0; b < NST && b < nb_total; ++b) issue(b);
   }
+  build_onehot(oh, lut, g);
 
   // lane columns: c0[k] + j, j = 0..3
   int c0[CPL];
@@ -338,21 +352,42 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
 #pragma unroll
       for (int i = 0; i < kGroup; ++i) acc[k][j][i] = 0u;
 
-  __syncthreads();  // oh[] and barriers ready
+  // table carries: sum the count slots above this segment (independent global
+  // loads, issued before the first barrier so they overlap the table build)
+  if (CARRY == CARRY_TABLE && s > 0) {
+    const int64_t plane_sz = (int64_t)a.nbp * a.Wp;
+    const uint16_t* cp = a.colpre + (f * a.nseg) * plane_sz + (int64_t)g * kGroup * a.Wp;
+    // prefix table: one slot; raw counts: sum slots 0..s-1 here (L2-resident),
+    // U slots' loads in flight at a time (register budget bounds U)
+    constexpr int U = CPL >= 4 ? 1 : 4;
+    const int sp0 = a.table_is_prefix ? s : 0;
+    const int sp1 = a.table_is_prefix ? s + 1 : s;
+    for (int sp = sp0; sp < sp1; sp += U) {
+      uint2 v[U][CPL][kGroup];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+#pragma unroll
+          for (int i = 0; i < kGroup; ++i)
+            v[u][k][i] = sp + u < sp1 ? *reinterpret_cast<const uint2*>(
+                                            cp + (sp + u) * plane_sz + i * a.Wp + c0[k])
+                                      : make_uint2(0u, 0u);
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int k = 0; k < CPL; ++k)
+#pragma unroll
+          for (int i = 0; i < kGroup; ++i) {
+            acc[k][0][i] += v[u][k][i].x & 0xffffu;
+            acc[k][1][i] += v[u][k][i].x >> 16;
+            acc[k][2][i] += v[u][k][i].y & 0xffffu;
+            acc[k][3][i] += v[u][k][i].y >> 16;
+          }
+    }
+  }
 
-  // ring batch b -> first row (pass 0 = counting, pass 1 = scan)
-  auto batch_row0 = [&](int b) { return rs + (int64_t)(b < nb_count ? b : b - nb_count) * R; };
-  auto issue = [&](int b) {  // producer: thread 0 only
-    const int stage = b % NST;
-    const int64_t r0 = batch_row0(b);
-    const int rows = (int)(re - r0 < R ? re - r0 : R);
-    mbar_expect_tx(&full_bar[stage], (uint32_t)rows * a.row_bytes);
-    for (int rr = 0; rr < rows; ++rr)
-      tma_row(ring + ((size_t)stage * R + rr) * a.Wp, img + (r0 + rr) * a.pitch, a.row_bytes,
-              &full_bar[stage]);
-  };
-  if (TMA && threadIdx.x == 0)
-    for (int b = 0; b < NST && b < nb_total; ++b) issue(b);
+  __syncthreads();  // oh[] and barriers ready
 
   // 4 one-hot words of lane columns c0[k]..+3 for row rr of ring batch b
   auto onehot4 = [&](int b, int rr, int k, uint32_t o[4]) {
@@ -470,37 +505,6 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
         __syncthreads();
         if (threadIdx.x == 0) st_release_gpu(flags + tile, kFlagIncl);
       }
-    }
-  } else if (CARRY == CARRY_TABLE && s > 0) {
-    const int64_t plane_sz = (int64_t)a.nbp * a.Wp;
-    const uint16_t* cp = a.colpre + (f * a.nseg) * plane_sz + (int64_t)g * kGroup * a.Wp;
-    // prefix table: one slot; raw counts: sum slots 0..s-1 here (L2-resident),
-    // U slots' loads in flight at a time (register budget bounds U)
-    constexpr int U = CPL >= 4 ? 1 : 4;
-    const int sp0 = a.table_is_prefix ? s : 0;
-    const int sp1 = a.table_is_prefix ? s + 1 : s;
-    for (int sp = sp0; sp < sp1; sp += U) {
-      uint2 v[U][CPL][kGroup];
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int k = 0; k < CPL; ++k)
-#pragma unroll
-          for (int i = 0; i < kGroup; ++i)
-            v[u][k][i] = sp + u < sp1 ? *reinterpret_cast<const uint2*>(
-                                            cp + (sp + u) * plane_sz + i * a.Wp + c0[k])
-                                      : make_uint2(0u, 0u);
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int k = 0; k < CPL; ++k)
-#pragma unroll
-          for (int i = 0; i < kGroup; ++i) {
-            acc[k][0][i] += v[u][k][i].x & 0xffffu;
-            acc[k][1][i] += v[u][k][i].x >> 16;
-            acc[k][2][i] += v[u][k][i].y & 0xffffu;
-            acc[k][3][i] += v[u][k][i].y >> 16;
-          }
     }
   }
 
