@@ -545,7 +545,12 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
   }
 
   // ---- pass 1: the scan
-  int64_t row_off = rs * W;  // element offset of the current row within a plane
+  // per-chunk pointer to this lane's 4 columns of the current row in bin 0's
+  // plane; bin i is `i * plane_elems` further.  Stepped by W per row.
+  uint32_t* prow[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) prow[k] = plane0 + rs * W + c0[k];
+  const bool full_group = nbins_here == kGroup;
   for (int b = nb_count; b < nb_total; ++b) {
     const int bi = b - nb_count;
     const int buf = bi & 1;
@@ -599,23 +604,28 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
           for (int i = 0; i < kGroup; ++i) run[i] += byte_of(ct[rr][k], i);
           const int c = c0[k];
           if (c < W) {
-            uint32_t* p = plane0 + row_off + c;
+            uint32_t* p = prow[k];
+            if (VEC && full_group) {
 #pragma unroll
-            for (int i = 0; i < kGroup; ++i) {
-              if (i < nbins_here) {
-                if (VEC) {
-                  st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
-                } else {
+              for (int i = 0; i < kGroup; ++i, p += plane_elems)
+                st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
+            } else {
 #pragma unroll
-                  for (int j = 0; j < 4; ++j)
-                    if (c + j < W) st_stream(p + j, acc[k][j][i]);
+              for (int i = 0; i < kGroup; ++i, p += plane_elems) {
+                if (i < nbins_here) {
+                  if (VEC) {
+                    st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
+                  } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                      if (c + j < W) st_stream(p + j, acc[k][j][i]);
+                  }
                 }
               }
-              p += plane_elems;
             }
           }
+          prow[k] += W;
         }
-        row_off += W;
       }
     }
   }
