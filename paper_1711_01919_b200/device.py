@@ -144,10 +144,11 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
             raise ShapeError("out has the wrong size or device")
     ws = _workspace_for(a, workspace)
     L = _native.lib()
-    _native.check(L.ih_integral_histogram(
-        a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
-        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
-        a.kernel, a.stream))
+    with torch.cuda.device(a.dev):  # launches go to the tensors' device
+        _native.check(L.ih_integral_histogram(
+            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+            a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
+            a.kernel, a.stream))
     if squeeze and out.dim() == 4:
         return out[0]
     return out
@@ -171,9 +172,11 @@ def prepare(images, table, bins, bin_range=None, kernel="auto", stream=None,
     scan (write-bound) runs."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
     ws = _workspace_for(a, workspace)
-    _native.check(_native.lib().ih_ih_prepare(
-        a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
-        a.bins, a.lo, a.hi, ws.data_ptr(), ws.numel() * ws.element_size(), a.kernel, a.stream))
+    with torch.cuda.device(a.dev):
+        _native.check(_native.lib().ih_ih_prepare(
+            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+            a.bins, a.lo, a.hi, ws.data_ptr(), ws.numel() * ws.element_size(), a.kernel,
+            a.stream))
 
 
 def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None,
@@ -181,10 +184,11 @@ def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None,
     """Phase 2 of integral_histogram (the dominant single-pass kernel)."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
     ws = _workspace_for(a, workspace)
-    _native.check(_native.lib().ih_ih_scan(
-        a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
-        a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
-        a.kernel, a.stream))
+    with torch.cuda.device(a.dev):
+        _native.check(_native.lib().ih_ih_scan(
+            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+            a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
+            a.kernel, a.stream))
     return out
 
 
@@ -217,9 +221,10 @@ def region_histograms(t: torch.Tensor, regions, stream=None) -> torch.Tensor:
     Q = int(regs.shape[0])
     out = torch.empty((Q, nb), dtype=torch.uint64, device=t.device)
     if Q:
-        _native.check(_native.lib().ih_region_histograms(
-            t.data_ptr(), nb, H, W, regs.data_ptr(), Q, out.data_ptr(),
-            _stream_handle(t.device, stream)))
+        with torch.cuda.device(t.device):
+            _native.check(_native.lib().ih_region_histograms(
+                t.data_ptr(), nb, H, W, regs.data_ptr(), Q, out.data_ptr(),
+                _stream_handle(t.device, stream)))
     return out
 
 
@@ -232,8 +237,10 @@ def window_counts(t: torch.Tensor, h: int, w: int, stream=None) -> torch.Tensor:
     if h > H or w > W:
         raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
     out = torch.empty((nb, H - h + 1, W - w + 1), dtype=torch.int64, device=t.device)
-    _native.check(_native.lib().ih_window_counts(
-        t.data_ptr(), nb, H, W, int(h), int(w), out.data_ptr(), _stream_handle(t.device, stream)))
+    with torch.cuda.device(t.device):
+        _native.check(_native.lib().ih_window_counts(
+            t.data_ptr(), nb, H, W, int(h), int(w), out.data_ptr(),
+            _stream_handle(t.device, stream)))
     return out
 
 
@@ -253,9 +260,10 @@ def likelihood_map(t: torch.Tensor, template, h: int, w: int, metric: str = "bha
     if h > H or w > W:
         raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
     out = torch.empty((H - h + 1, W - w + 1), dtype=torch.float64, device=t.device)
-    _native.check(_native.lib().ih_likelihood_map(
-        t.data_ptr(), nb, H, W, int(h), int(w), tmpl.ctypes.data, metrics[metric],
-        out.data_ptr(), _stream_handle(t.device, stream)))
+    with torch.cuda.device(t.device):
+        _native.check(_native.lib().ih_likelihood_map(
+            t.data_ptr(), nb, H, W, int(h), int(w), tmpl.ctypes.data, metrics[metric],
+            out.data_ptr(), _stream_handle(t.device, stream)))
     return out
 
 
