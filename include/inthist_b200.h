@@ -52,7 +52,7 @@ typedef enum {
 /* Kernel family used by ih_integral_histogram.  Results are bit-identical
  * for every choice (the reference's contract). */
 typedef enum {
-    IH_KERNEL_AUTO = 0,         /* single-pass scan when the width allows, else cross-weave */
+    IH_KERNEL_AUTO = 0,         /* single-pass scan (column-tiled beyond 2048 columns) */
     IH_KERNEL_SINGLE_PASS = 1,  /* K2: fused bin + 2D scan, each output byte written once */
     IH_KERNEL_CROSSWEAVE = 2    /* K1 + K1b: fused bin/row scan, then column scan (CW-B) */
 } ih_kernel;
@@ -104,7 +104,8 @@ ih_status ih_ih_scan(const uint8_t *img, int64_t frames, int64_t height, int64_t
  *   info[2] row segments per frame           info[3] rows per segment
  *   info[4] 128-column chunks per lane       info[5] rows per barrier batch
  *   info[6] warps per CTA                    info[7] workspace bytes needed
- * Same shape/parameter errors as ih_integral_histogram. */
+ *   info[8] column tiles per row             info[9] tile width (columns)
+ * (`info` holds 10 entries.)  Same shape/parameter errors as ih_integral_histogram. */
 ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
                            int32_t kernel, int32_t aligned16, int64_t *info);
 

@@ -44,7 +44,10 @@ struct K2Plan {
   int nbp = 0;       // padded slab bins
   int nseg = 1;      // row segments per frame
   int S = 0;         // rows per segment
-  int64_t Wp = 0;    // padded width = nwarps * cpl * 128
+  int64_t Wp = 0;    // padded width = T * TW
+  int T = 1;         // column tiles (colt)
+  int TW = 0;        // tile width = nwarps * cpl * 128
+  bool colt = false; // column-tiled instantiation (W > 2048 unless IH_NO_COLTILE)
   int carry = 0;     // ih::Carry: NONE (nseg == 1), TABLE or LOOKBACK
   bool big = false;  // 1024-thread instantiation (up to 32 warps, <= 64 registers)
   bool vec = true;   // W % 4 == 0
@@ -54,24 +57,31 @@ struct K2Plan {
 using K2Fn = void (*)(ih::ScanArgs, ih::RelLut);
 
 template <int CPL, int R, bool VEC, bool TMA, int MAXT>
-K2Fn pick_carry(int carry) {
+K2Fn pick_carry(int carry, bool colt) {
+  if constexpr (CPL == 1 && MAXT == 512) {  // column tiles: CPL 1, table carries
+    if (colt)
+      return carry == ih::CARRY_TABLE ? ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_TABLE, MAXT, true>
+             : carry == ih::CARRY_NONE ? ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_NONE, MAXT, true>
+                                       : nullptr;
+  }
+  if (colt) return nullptr;
   switch (carry) {
-    case ih::CARRY_TABLE: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_TABLE, MAXT>;
-    case ih::CARRY_LOOKBACK: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_LOOKBACK, MAXT>;
-    default: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_NONE, MAXT>;
+    case ih::CARRY_TABLE: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_TABLE, MAXT, false>;
+    case ih::CARRY_LOOKBACK: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_LOOKBACK, MAXT, false>;
+    default: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_NONE, MAXT, false>;
   }
 }
 template <int CPL, int R>
 K2Fn pick_vt(const K2Plan& p) {
   if constexpr (CPL == 1) {  // 1024-thread variants: CPL 1, aligned fast path only
-    if (p.big) return pick_carry<CPL, R, true, true, 1024>(p.carry);
+    if (p.big) return pick_carry<CPL, R, true, true, 1024>(p.carry, false);
   } else {
     if (p.big) return nullptr;
   }
-  if (p.vec && p.tma) return pick_carry<CPL, R, true, true, 512>(p.carry);
-  if (p.vec) return pick_carry<CPL, R, true, false, 512>(p.carry);
-  if (p.tma) return pick_carry<CPL, R, false, true, 512>(p.carry);
-  return pick_carry<CPL, R, false, false, 512>(p.carry);
+  if (p.vec && p.tma) return pick_carry<CPL, R, true, true, 512>(p.carry, p.colt);
+  if (p.vec) return pick_carry<CPL, R, true, false, 512>(p.carry, p.colt);
+  if (p.tma) return pick_carry<CPL, R, false, true, 512>(p.carry, p.colt);
+  return pick_carry<CPL, R, false, false, 512>(p.carry, p.colt);
 }
 // The instantiated (CPL, R) pairs; plan_k2 only produces these.
 K2Fn pick_k2(const K2Plan& p) {
@@ -88,7 +98,7 @@ K2Fn pick_k2(const K2Plan& p) {
 size_t k2_ring_smem(const K2Plan& p) {
   if (!p.tma) return 0;
   const int nst = p.R >= 4 ? 2 : (p.R == 2 ? 4 : 8);  // ih::Ring<R>::kStages
-  return (size_t)nst * p.R * p.Wp;
+  return (size_t)nst * p.R * p.TW;
 }
 
 // Resident CTAs per SM for the plan's kernel (occupancy API); a register-based
@@ -114,7 +124,12 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   p.vec = vec;
   p.tma = tma;
   const int64_t nchunks = (W + ih::kChunk - 1) / ih::kChunk;
-  if (vec && tma && env_int("IH_NO_BIG", 0) == 0 && nchunks > 16 && nchunks <= 32) {
+  if (nchunks > 16 && env_int("IH_NO_COLTILE", 0) == 0) {
+    // W > 2048: column tiles of <= 16 chunks (CPL 1), as even as possible
+    p.colt = true;
+    p.cpl = 1;
+    p.T = (int)((nchunks + 15) / 16);
+  } else if (vec && tma && env_int("IH_NO_BIG", 0) == 0 && nchunks > 16 && nchunks <= 32) {
     // W in (2048, 4096]: one 1024-thread CTA per SM, CPL 1 at <= 64 registers
     p.big = true;
     p.cpl = 1;
@@ -127,8 +142,10 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   } else {
     return p;  // cpl = 0: use the cross-weave kernels
   }
-  p.nwarps = (int)((nchunks + p.cpl - 1) / p.cpl);
-  p.Wp = (int64_t)p.nwarps * p.cpl * ih::kChunk;
+  const int64_t tchunks = (nchunks + p.T - 1) / p.T;  // chunks per column tile
+  p.nwarps = (int)((tchunks + p.cpl - 1) / p.cpl);
+  p.TW = p.nwarps * p.cpl * ih::kChunk;
+  p.Wp = (int64_t)p.T * p.TW;
   // rows per barrier batch: tuned on B200 (scripts/sweep*.py, profiles/); the
   // caps keep the accumulators + batch state inside the register budget
   p.R = p.cpl == 1 ? 4 : p.cpl == 2 ? 2 : 1;
@@ -146,7 +163,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   // the minimum segment height caps the count, snap down to whole waves.
   // Each segment costs a u16 count slot of 1/(2S) of the output (mostly L2).
   const int64_t slots = (int64_t)kNumSMs * ctas_per_sm(p);
-  const int64_t units = frames * p.ngroups;
+  const int64_t units = frames * p.ngroups * p.T;
   const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", 32);
   const int64_t max_seg = (H + min_rows - 1) / min_rows;
   const bool many = units * 4 >= slots;  // >= a quarter wave without segments
@@ -155,10 +172,10 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (w_env > 0) waves = w_env / 10.0;
   const double raw = waves * (double)slots / (double)units;
   int64_t nseg;
-  if (raw <= (double)max_seg && slots == kNumSMs) {
-    // one CTA per SM: a partial last wave idles whole SMs for a CTA's
-    // lifetime; pick the count in [raw/2, 2*raw] that leaves the fewest idle
-    // slots (ties: fewer segments)
+  if (raw <= (double)max_seg && (slots == kNumSMs || (p.colt && !many))) {
+    // one CTA per SM, or few waves of column tiles: a partial last wave idles
+    // whole SMs for a CTA's lifetime; pick the count in [raw/2, 2*raw] that
+    // leaves the fewest idle slots (ties: fewer segments)
     int64_t best = 1;
     double best_idle = 2.0;
     const int64_t lo = (int64_t)(raw / 2) > 1 ? (int64_t)(raw / 2) : 1;
@@ -191,6 +208,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (nseg > 1 && p.S > 65535) p.S = 65535;
   p.nseg = (int)((H + p.S - 1) / p.S);
   if (p.nseg <= 1) p.carry = ih::CARRY_NONE;
+  else if (p.colt) p.carry = ih::CARRY_TABLE;
   else p.carry = env_int("IH_CARRY_LOOKBACK", 0) ? ih::CARRY_LOOKBACK : ih::CARRY_TABLE;
   return p;
 }
@@ -215,7 +233,23 @@ int64_t lb_tiles(int64_t frames, const K2Plan& p) { return frames * p.ngroups * 
 size_t lb_header_bytes(int64_t frames, const K2Plan& p) {
   return 16 + (size_t)((lb_tiles(frames, p) * 4 + 15) / 16 * 16);
 }
-size_t k2_ws_bytes(int64_t frames, const K2Plan& p) {
+//   column tiles:   [CARRY_TABLE table, 256 B aligned][rowleft: (frames, T-1, H, nbp) u32]
+//                   [segleft: (frames, nseg, T-1, nbp) u32, when nseg > 1]
+size_t k2_table_bytes(int64_t frames, const K2Plan& p) {
+  if (p.carry != ih::CARRY_TABLE) return 0;
+  return ((size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint16_t) + 255) / 256 * 256;
+}
+size_t k2_rowleft_bytes(int64_t frames, int64_t H, const K2Plan& p) {
+  if (!p.colt || p.T < 2) return 0;
+  return (size_t)frames * (p.T - 1) * H * p.nbp * sizeof(uint32_t);
+}
+size_t k2_segleft_bytes(int64_t frames, const K2Plan& p) {
+  if (!p.colt || p.T < 2 || p.nseg < 2) return 0;
+  return (size_t)frames * p.nseg * (p.T - 1) * p.nbp * sizeof(uint32_t);
+}
+size_t k2_ws_bytes(int64_t frames, int64_t H, const K2Plan& p) {
+  if (p.colt)
+    return k2_table_bytes(frames, p) + k2_rowleft_bytes(frames, H, p) + k2_segleft_bytes(frames, p);
   if (p.carry == ih::CARRY_TABLE) return (size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint16_t);
   if (p.carry == ih::CARRY_LOOKBACK)
     return lb_header_bytes(frames, p) +
@@ -271,7 +305,7 @@ ih_status validate(const uint8_t* img, int64_t frames, int64_t H, int64_t W, int
   c->plan = plan_k2(frames, H, W, c->nb, W % 4 == 0, tma);
   c->kernel = resolve_kernel(kernel, c->plan);
   if (c->kernel == IH_KERNEL_SINGLE_PASS && c->plan.cpl == 0)
-    return fail(IH_ERR_PARAM, "single-pass kernel supports width <= 8192; use crossweave");
+    return fail(IH_ERR_PARAM, "single-pass kernel without column tiles supports width <= 8192; use crossweave");
   return IH_OK;
 }
 
@@ -280,19 +314,54 @@ bool aligned_rows(const Call& c) {
 }
 
 
+ih_status launch_colprefix(const Call& c, void* ws);
+
 ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
-  if (c.kernel != IH_KERNEL_SINGLE_PASS || c.plan.carry == ih::CARRY_NONE) return IH_OK;
+  if (c.kernel != IH_KERNEL_SINGLE_PASS) return IH_OK;
   const K2Plan& p = c.plan;
-  if (ws_bytes < k2_ws_bytes(c.frames, p) || !ws)
+  const size_t need = k2_ws_bytes(c.frames, c.H, p);
+  if (need == 0) return IH_OK;
+  if (ws_bytes < need || !ws)
     return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
+  if (p.colt && p.T > 1) {  // row counts left of each tile boundary (+ per-segment sums)
+    uint32_t* lc = (uint32_t*)((uint8_t*)ws + k2_table_bytes(c.frames, p));
+    uint32_t* sl = nullptr;
+    if (k2_segleft_bytes(c.frames, p)) {
+      sl = (uint32_t*)((uint8_t*)lc + k2_rowleft_bytes(c.frames, c.H, p));
+      if (cudaMemsetAsync(sl, 0, k2_segleft_bytes(c.frames, p), c.stream) != cudaSuccess)
+        return cuda_fail("segleft reset");
+    }
+    dim3 grid((unsigned)((c.H + ih::kRowLeftWarps - 1) / ih::kRowLeftWarps), (unsigned)c.frames);
+    if (aligned_rows(c))
+      ih::k2_rowleft<true><<<grid, ih::kRowLeftWarps * 32, 0, c.stream>>>(
+          c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.nbp, p.T, p.TW, p.S, p.nseg, lc, sl);
+    else
+      ih::k2_rowleft<false><<<grid, ih::kRowLeftWarps * 32, 0, c.stream>>>(
+          c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.nbp, p.T, p.TW, p.S, p.nseg, lc, sl);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_rowleft");
+  }
+  if (p.carry == ih::CARRY_NONE) return IH_OK;
   if (p.carry == ih::CARRY_LOOKBACK) {  // reset the ticket and the tile flags
     if (cudaMemsetAsync(ws, 0, lb_header_bytes(c.frames, p), c.stream) != cudaSuccess)
       return cuda_fail("look-back flag reset");
     return IH_OK;
   }
+  const bool al = aligned_rows(c);
+  if (env_int("IH_COLCOUNTS_SLAB", 0) == 0) {  // all bins in one pass (shared atomics)
+    dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
+    auto kern = al ? ih::k2_colcounts_all<true> : ih::k2_colcounts_all<false>;
+    const size_t smem = (size_t)p.nbp * 64 * sizeof(uint32_t);
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+            cudaSuccess)
+      return cuda_fail("k2_colcounts_all smem attribute");
+    kern<<<grid, 256, smem, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S, p.nseg,
+                                        p.nbp, p.Wp, (uint16_t*)ws);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts_all");
+    return launch_colprefix(c, ws);
+  }
   const int nslab = (p.nbp + ih::kCountSlab - 1) / ih::kCountSlab;
   dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)(c.frames * nslab));
-  const bool al = aligned_rows(c);
   // warps per colcounts CTA: ~48+ rows per warp, 2..8 warps
   const int nw = p.S >= 384 ? 8 : p.S >= 192 ? 4 : 2;
   auto kern = al ? (nw == 8 ? ih::k2_colcounts<true, 8>
@@ -307,6 +376,11 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
   kern<<<grid, nw * 32, smem, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S, p.nseg,
                                           p.nbp, p.Wp, nslab, (uint16_t*)ws);
   if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts");
+  return launch_colprefix(c, ws);
+}
+
+ih_status launch_colprefix(const Call& c, void* ws) {
+  const K2Plan& p = c.plan;
   if (!table_prefix_h(p, c.H)) return IH_OK;  // the scan kernel sums the count slots
   const int64_t total = c.frames * p.nbp * p.Wp / 4 * ih::kPrefixLanes;  // 8 lanes per quad
   int64_t blocks = (total + 255) / 256;
@@ -354,7 +428,7 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
     return IH_OK;
   }
   const K2Plan& p = c.plan;
-  if (p.carry != ih::CARRY_NONE && (ws_bytes < k2_ws_bytes(c.frames, p) || !ws))
+  if (k2_ws_bytes(c.frames, c.H, p) > 0 && (ws_bytes < k2_ws_bytes(c.frames, c.H, p) || !ws))
     return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
   ih::ScanArgs a;
   a.img = c.img;
@@ -367,7 +441,14 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
   a.S = p.S;
   a.nseg = p.nseg;
   a.Wp = p.Wp;
+  a.T = p.T;
+  a.TW = p.TW;
   a.row_bytes = (uint32_t)((c.W + 15) / 16 * 16);
+  a.rowleft = p.colt && p.T > 1 ? (const uint32_t*)((const uint8_t*)ws + k2_table_bytes(c.frames, p))
+                                : nullptr;
+  a.segleft = k2_segleft_bytes(c.frames, p)
+                  ? (const uint32_t*)((const uint8_t*)a.rowleft + k2_rowleft_bytes(c.frames, c.H, p))
+                  : nullptr;
   a.colpre = p.carry == ih::CARRY_TABLE ? (const uint16_t*)ws : nullptr;
   a.table_is_prefix = table_prefix_h(p, c.H) ? 1 : 0;
   a.lb_ticket = a.lb_flags = a.lb_agg = a.lb_incl = nullptr;
@@ -379,7 +460,7 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
     a.lb_incl = a.lb_agg + lb_tiles(c.frames, p) * ih::kGroup * p.Wp;
   }
   a.out = out;
-  dim3 grid((unsigned)p.ngroups, (unsigned)p.nseg, (unsigned)c.frames);
+  dim3 grid((unsigned)(p.ngroups * p.T), (unsigned)p.nseg, (unsigned)c.frames);
   const int threads = p.nwarps * 32;
   return launch_k2(c, a, grid, threads);
 }
@@ -398,7 +479,7 @@ size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width, int32_t
     K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0 && (variant & 1),
                        (variant & 2) != 0);
     if (resolve_kernel(kernel, p) != IH_KERNEL_SINGLE_PASS || p.cpl == 0) continue;
-    const size_t b = k2_ws_bytes(frames, p);
+    const size_t b = k2_ws_bytes(frames, height, p);
     if (b > n) n = b;
   }
   return n;
@@ -486,7 +567,7 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   const bool tma = aligned16 != 0 && env_int("IH_NO_TMA", 0) == 0;
   K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0, tma);
   const int k = resolve_kernel(kernel, p);
-  for (int i = 0; i < 8; ++i) info[i] = 0;
+  for (int i = 0; i < 10; ++i) info[i] = 0;
   info[0] = k;
   if (k == IH_KERNEL_CROSSWEAVE) {
     info[1] = height > 1 ? 2 : 1;
@@ -495,13 +576,16 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   if (p.cpl == 0) return fail(IH_ERR_PARAM, "single-pass kernel supports width <= 8192");
   int launches = 1;
   if (p.carry == ih::CARRY_TABLE) launches += table_prefix_h(p, height) ? 2 : 1;
+  if (p.colt && p.T > 1) launches += 1;  // k2_rowleft
   info[1] = launches;
   info[2] = p.nseg;
   info[3] = p.S;
   info[4] = p.cpl;
   info[5] = p.R;
   info[6] = p.nwarps;
-  info[7] = (int64_t)k2_ws_bytes(frames, p);
+  info[7] = (int64_t)k2_ws_bytes(frames, height, p);
+  info[8] = p.T;
+  info[9] = p.TW;
   return IH_OK;
 }
 
@@ -543,6 +627,6 @@ const char* ih_status_string(ih_status s) {
 
 const char* ih_last_error(void) { return g_last_error; }
 
-int32_t ih_abi_version(void) { return (1 << 16) | 0; }
+int32_t ih_abi_version(void) { return (1 << 16) | 1; }
 
 }  // extern "C"

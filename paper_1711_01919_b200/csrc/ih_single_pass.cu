@@ -129,6 +129,83 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
 }
 
 // ---------------------------------------------------------------------------
+// k2_colcounts_all: the same table for ALL slab bins in one pass (one read and
+// one count per pixel instead of one per 32-bin slab).  CTA = (128-column
+// chunk, segment, frame); NW warps stride the segment's rows (8 rows of loads
+// in flight per warp) and count into ONE shared histogram with 32-bit shared
+// atomics.  Word (b, h, lane) packs the 16-bit counts of columns 4*lane+2h
+// (low half) and 4*lane+2h+1 (high half): increments are 1 << 16*(k&1), and
+// the bank is the lane, so a warp's atomics never conflict.  Counts per
+// segment are < 65536 (host-enforced), so halves never carry.  The dump is
+// directly the u16x4 layout of the table.
+// ---------------------------------------------------------------------------
+template <bool ALIGNED>
+__global__ void __launch_bounds__(256) k2_colcounts_all(
+    const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
+    RelLut lut, int S, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws) {
+  extern __shared__ __align__(16) uint32_t hist2[];  // [nbp][2][32]
+  __shared__ uint32_t sw[512];  // pixel (| 256 past the edge) -> word offset of its bin, or ~0
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int nw = blockDim.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * kChunk + 4 * lane;
+  const int s = blockIdx.y;
+  const int64_t f = blockIdx.z;
+  for (int v = threadIdx.x; v < 512; v += blockDim.x) {
+    const uint32_t b = v < 256 ? (uint32_t)lut.rel[v] : 0xffffffffu;
+    sw[v] = b < (uint32_t)nbp ? b * 64u : 0xffffffffu;
+  }
+  {
+    uint4* z = reinterpret_cast<uint4*>(hist2);
+    for (int i = threadIdx.x; i < nbp * 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+  }
+  uint32_t inval[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) inval[k] = (c + k < W) ? 0u : 256u;
+  __syncthreads();
+  uint32_t* hl = hist2 + lane;
+  const uint8_t* base = img + f * fstride;
+  const int64_t seg0 = (int64_t)s * S;
+  const int64_t seg1 = (seg0 + S < H ? seg0 + S : H);
+  auto load_px = [&](int64_t r) -> uint32_t {
+    const uint8_t* row = base + r * pitch + c;
+    if (ALIGNED) return __ldg(reinterpret_cast<const uint32_t*>(row));
+    uint32_t px = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+      if (c + k < W) px |= (uint32_t)__ldg(row + k) << (8 * k);
+    return px;
+  };
+  auto count4 = [&](uint32_t px) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t o = sw[((px >> (8 * k)) & 0xffu) | inval[k]];
+      if (o != 0xffffffffu) atomicAdd(hl + o + (k >> 1) * 32, 1u << (16 * (k & 1)));
+    }
+  };
+  if (c < W) {
+    // rows seg0 + warp + i*nw; 8 rows of loads in flight per warp
+    constexpr int U = 8;
+    const int64_t step = (int64_t)nw * U;
+    for (int64_t r = seg0 + warp; r < seg1; r += step) {
+      uint32_t px[U];
+#pragma unroll
+      for (int i = 0; i < U; ++i) px[i] = r + i * nw < seg1 ? load_px(r + i * nw) : 0u;
+#pragma unroll
+      for (int i = 0; i < U; ++i)
+        if (r + i * nw < seg1) count4(px[i]);
+    }
+  }
+  __syncthreads();
+  uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp) * Wp + (int64_t)blockIdx.x * kChunk;
+  for (int e = threadIdx.x; e < nbp * 32; e += blockDim.x) {
+    const int l = e & 31, b = e >> 5;
+    *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) =
+        make_uint2(hist2[(b * 2) * 32 + l], hist2[(b * 2 + 1) * 32 + l]);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k2_colprefix: in place, ws[f][s][b][c] <- sum_{s' < s} counts[f][s'][b][c]
 // (u16; only used when H <= 65535 so every prefix fits).  Thread per
 // (f, b, 4 columns); loads are issued 8 segments at a time before any store.
@@ -181,6 +258,79 @@ __global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, i
 }
 
 // ---------------------------------------------------------------------------
+// k2_rowleft: column-tile row carries for the COLT scan.
+//   lc[f][t][r][b] = #{ c < (t+1)*TW : Q(I(r,c)) = b },  t < T-1, b < nbp  (u32)
+// i.e. H_b restricted to row r at the last column left of tile t+1, and
+//   sl[f][s][t][b] += lc[f][t][r][b] over the rows r of segment s < nseg-1
+// (zeroed by the host first) -- the part of the segment carry H_b(r_s-1, .)
+// left of a tile.  Warp per row walking the row left to right (one 32-bit
+// pixel load per lane per 128-column chunk, 16 chunks of loads in flight)
+// into a warp-private shared histogram; the histogram is cumulative, so at
+// each tile boundary it is dumped as is (coalesced, one u32 per bin).
+// ---------------------------------------------------------------------------
+constexpr int kRowLeftWarps = 8;
+
+template <bool ALIGNED>
+__global__ void __launch_bounds__(kRowLeftWarps * 32) k2_rowleft(
+    const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
+    RelLut lut, int nbp, int T, int TW, int S, int nseg, uint32_t* __restrict__ lc,
+    uint32_t* __restrict__ sl) {
+  __shared__ uint32_t hist[kRowLeftWarps][256];
+  __shared__ uint8_t rel[256];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  for (int v = threadIdx.x; v < 256; v += blockDim.x) rel[v] = lut.rel[v];
+  for (int v = lane; v < 256; v += 32) hist[warp][v] = 0u;
+  __syncthreads();
+  const int64_t r = (int64_t)blockIdx.x * kRowLeftWarps + warp;
+  const int64_t f = blockIdx.y;
+  if (r >= H) return;
+  const uint8_t* row = img + f * fstride + r * pitch;
+  uint32_t* h = hist[warp];
+  auto load_px = [&](int64_t c) -> uint32_t {  // columns < (T-1)*TW < W: always in range
+    if (ALIGNED) return __ldg(reinterpret_cast<const uint32_t*>(row + c));
+    uint32_t px = 0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) px |= (uint32_t)__ldg(row + c + k) << (8 * k);
+    return px;
+  };
+  auto count4 = [&](uint32_t px) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      // rel = 0xff marks "outside the slab" unless the slab has 256 bins (then
+      // it is bin 255); either way only bins < nbp are counted (a marker pixel
+      // with nbp == 256 lands in padding bin 255, which is never stored)
+      const uint32_t b = rel[(px >> (8 * k)) & 0xffu];
+      if (b < (uint32_t)nbp) atomicAdd(&h[b], 1u);
+    }
+  };
+  const int cpt = TW / kChunk;  // chunks per tile
+  const int64_t s = r / S;
+  const bool seg_sum = sl != nullptr && s + 1 < nseg;
+  constexpr int U = 16;
+  for (int t = 0; t + 1 < T; ++t) {
+    const int64_t cb = (int64_t)t * TW + 4 * lane;
+    for (int k0 = 0; k0 < cpt; k0 += U) {
+      uint32_t px[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) px[u] = k0 + u < cpt ? load_px(cb + (int64_t)(k0 + u) * kChunk) : 0u;
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+        if (k0 + u < cpt) count4(px[u]);
+    }
+    __syncwarp();
+    uint32_t* dst = lc + (((f * (T - 1) + t) * H) + r) * (int64_t)nbp;
+    uint32_t* sdst = sl + ((f * nseg + s) * (T - 1) + t) * (int64_t)nbp;
+    for (int b = lane; b < nbp; b += 32) {
+      const uint32_t v = h[b];
+      dst[b] = v;
+      if (seg_sum && v) atomicAdd(sdst + b, v);
+    }
+    __syncwarp();
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k2_scan: the single pass.  Template parameters:
 //   CPL  chunks per lane (warp covers CPL*128 columns)
 //   R    rows per barrier batch
@@ -188,6 +338,9 @@ __global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, i
 //   TMA  image rows 16-byte aligned: rows are staged into a shared-memory ring
 //        by cp.async.bulk (TMA bulk copies, mbarrier completion), NST batches
 //        ahead of the consumers; otherwise lanes load pixels with LDG.
+//   COLT column tiles: the CTA covers columns [t*TW, (t+1)*TW) of the row;
+//        rows get the counts left of the tile from k2_rowleft, the segment
+//        carry adds k2_rowleft's per-segment sums of those over the segments above.
 // ---------------------------------------------------------------------------
 struct ScanArgs {
   const uint8_t* img;
@@ -195,8 +348,12 @@ struct ScanArgs {
   int nb;          // slab bins (bin_hi - bin_lo)
   int nbp;         // padded to a multiple of 4
   int S, nseg;     // segment rows, segments per frame
-  int64_t Wp;      // padded width (multiple of 128) = row stride of the smem ring
-  uint32_t row_bytes;      // bytes copied per row by TMA = round_up(W, 16)
+  int64_t Wp;      // padded width = T * TW (row stride of the carry tables)
+  int T;           // column tiles per row (COLT kernels; 1 otherwise)
+  int TW;          // tile width = warps * CPL * 128 = row stride of the smem ring
+  uint32_t row_bytes;      // bytes copied per row by TMA = round_up(W, 16) (T == 1)
+  const uint32_t* rowleft; // COLT: (frames, T-1, H, nbp) u32 row counts left of tile t+1
+  const uint32_t* segleft; // COLT: (frames, nseg, T-1, nbp) u32 their sums per segment
   const uint16_t* colpre;  // CARRY_TABLE: (frames, nseg, nbp, Wp) u16 column counts or prefixes
   int table_is_prefix;     // 1: slot s holds sum_{s'<s} counts (k2_colprefix ran); 0: raw counts
   uint32_t* lb_ticket;     // CARRY_LOOKBACK: tile ticket counter (zeroed per launch)
@@ -270,11 +427,15 @@ __device__ __forceinline__ uint32_t warp_scan_pred(uint32_t x) {
 
 // MAXT: launch bound -- 512 (<= 16 warps, up to 128 registers) or 1024
 // (<= 32 warps at <= 64 registers: full SM occupancy from one CTA).
-template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT>
-__global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
+// COLT kernels must keep two 16-warp CTAs per SM (<= 64 registers).
+template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT, bool COLT>
+__global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut lut) {
   constexpr int NST = Ring<R>::kStages;
+  static_assert(!(COLT && CARRY == CARRY_LOOKBACK), "column tiles use table carries");
   __shared__ uint32_t oh[kOneHotEntries];
   __shared__ uint4 tot[2][R][32];
+  __shared__ uint4 sleft[2][COLT ? R : 1];  // COLT: per-row counts left of the tile
+  __shared__ uint4 sls[1];                  // COLT: carry part left of the tile
   __shared__ __align__(8) uint64_t full_bar[NST];
   __shared__ uint32_t s_tile, s_flag;
   extern __shared__ __align__(128) uint8_t ring[];  // [NST][R][Wp] image rows (TMA)
@@ -286,7 +447,7 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
   // Tile (frame f, bin group g, segment s).  With look-back carries the tile
   // comes from an atomic ticket, so every tile a CTA waits on has already
   // started (forward progress); segments of one (f, g) chain are adjacent.
-  int g, s;
+  int g, s, t = 0;
   int64_t f;
   if (CARRY == CARRY_LOOKBACK) {
     if (threadIdx.x == 0) s_tile = atomicAdd(a.lb_ticket, 1u);
@@ -296,11 +457,20 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
     g = (int)((t / (uint32_t)a.nseg) % (uint32_t)gridDim.x);
     f = (int64_t)(t / ((uint32_t)a.nseg * gridDim.x));
   } else {
-    g = blockIdx.x;
+    if (COLT) {
+      g = (int)(blockIdx.x / (unsigned)a.T);
+      t = (int)(blockIdx.x % (unsigned)a.T);
+    } else {
+      g = blockIdx.x;
+    }
     s = blockIdx.y;
     f = blockIdx.z;
   }
   const uint8_t* img = a.img + f * a.fstride;
+  const int64_t ct = COLT ? (int64_t)t * a.TW : 0;  // first column of the tile
+  // TMA bytes per row: the tile's columns rounded up to 16 (inside the pitched row)
+  const uint32_t row_bytes =
+      COLT ? (uint32_t)min((int64_t)a.TW, (W - ct + 15) / 16 * 16) : a.row_bytes;
   const int64_t rs = (int64_t)s * a.S;
   const int64_t re = (rs + a.S < H ? rs + a.S : H);
   const int nbatch = (int)((re - rs + R - 1) / R);
@@ -315,9 +485,9 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
     const int stage = b % NST;
     const int64_t r0 = batch_row0(b);
     const int rows = (int)(re - r0 < R ? re - r0 : R);
-    mbar_expect_tx(&full_bar[stage], (uint32_t)rows * a.row_bytes);
+    mbar_expect_tx(&full_bar[stage], (uint32_t)rows * row_bytes);
     for (int rr = 0; rr < rows; ++rr)
-      tma_row(ring + ((size_t)stage * R + rr) * a.Wp, img + (r0 + rr) * a.pitch, a.row_bytes,
+      tma_row(ring + ((size_t)stage * R + rr) * a.TW, img + (r0 + rr) * a.pitch + ct, row_bytes,
               &full_bar[stage]);
   };
   // start the image stream first: the ring fill overlaps the table build below
@@ -329,18 +499,21 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
   }
   build_onehot(oh, lut, g);
 
-  // lane columns: c0[k] + j, j = 0..3
-  int c0[CPL];
+  // lane columns: ct + cl[k] + j, j = 0..3 (cl = column inside the tile)
+  int cl[CPL];
   uint32_t inval[CPL][4];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) {
-    c0[k] = (warp * CPL + k) * kChunk + lane * 4;
+    cl[k] = (warp * CPL + k) * kChunk + lane * 4;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) inval[k][j] = (c0[k] + j < W) ? 0u : 256u;
+    for (int j = 0; j < 4; ++j) inval[k][j] = (ct + cl[k] + j < W) ? 0u : 256u;
   }
 
   // output: bin i of this group at plane0 + i * plane_stride (bins >= nb masked)
   const int64_t plane_elems = H * W;
+  bool colok[CPL];
+#pragma unroll
+  for (int k = 0; k < CPL; ++k) colok[k] = ct + cl[k] < W;
   uint32_t* plane0 = a.out + (f * a.nb + (int64_t)g * kGroup) * plane_elems;
   const int nbins_here = min(kGroup, a.nb - g * kGroup);
 
@@ -371,7 +544,7 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
 #pragma unroll
           for (int i = 0; i < kGroup; ++i)
             v[u][k][i] = sp + u < sp1 ? *reinterpret_cast<const uint2*>(
-                                            cp + (sp + u) * plane_sz + i * a.Wp + c0[k])
+                                            cp + (sp + u) * plane_sz + i * a.Wp + ct + cl[k])
                                       : make_uint2(0u, 0u);
 #pragma unroll
       for (int u = 0; u < U; ++u)
@@ -385,20 +558,48 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
             acc[k][3][i] += v[u][k][i].y >> 16;
           }
     }
+    if (COLT && t > 0 && warp == 0) {
+      // the carry also counts the pixels above the segment and left of the
+      // tile: sum over segments s' < s of k2_rowleft's per-segment sums
+      uint4 part = make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t* sl = a.segleft + (f * a.nseg * (a.T - 1) + (t - 1)) * a.nbp + g * kGroup;
+      for (int sp = lane; sp < s; sp += 32) {
+        const uint4 x = __ldg(reinterpret_cast<const uint4*>(sl + (int64_t)sp * (a.T - 1) * a.nbp));
+        part.x += x.x;
+        part.y += x.y;
+        part.z += x.z;
+        part.w += x.w;
+      }
+      part.x = __reduce_add_sync(kFull, part.x);
+      part.y = __reduce_add_sync(kFull, part.y);
+      part.z = __reduce_add_sync(kFull, part.z);
+      part.w = __reduce_add_sync(kFull, part.w);
+      if (lane == 0) sls[0] = part;
+    }
+  }
+
+  // COLT: row counts left of the tile (k2_rowleft), prefetched one batch ahead
+  // by lanes 0..R-1 of warp 0 and handed to the CTA through sleft[]
+  const uint32_t* lrow = nullptr;
+  uint4 lnext = make_uint4(0u, 0u, 0u, 0u);
+  if (COLT && t > 0) {
+    lrow = a.rowleft + ((f * (a.T - 1) + (t - 1)) * H) * a.nbp + g * kGroup;
+    if (warp == 0 && lane < R && rs + lane < re)
+      lnext = __ldg(reinterpret_cast<const uint4*>(lrow + (rs + lane) * a.nbp));
   }
 
   __syncthreads();  // oh[] and barriers ready
 
-  // 4 one-hot words of lane columns c0[k]..+3 for row rr of ring batch b
+  // 4 one-hot words of lane columns cl[k]..+3 for row rr of ring batch b
   auto onehot4 = [&](int b, int rr, int k, uint32_t o[4]) {
     if (TMA) {
       const int stage = b % NST;
       const uint32_t px = *reinterpret_cast<const uint32_t*>(
-          ring + ((size_t)stage * R + rr) * a.Wp + c0[k]);
+          ring + ((size_t)stage * R + rr) * a.TW + cl[k]);
 #pragma unroll
       for (int j = 0; j < 4; ++j) o[j] = oh[((px >> (8 * j)) & 0xffu) | inval[k][j]];
     } else {
-      load_onehot4<false>(img + (batch_row0(b) + rr) * a.pitch, c0[k], W, oh, inval[k], o);
+      load_onehot4<false>(img + (batch_row0(b) + rr) * a.pitch, ct + cl[k], W, oh, inval[k], o);
     }
   };
 
@@ -451,12 +652,12 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
         }
 #pragma unroll
         for (int i = 0; i < kGroup; ++i)
-          __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + c0[k]),
+          __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + cl[k]),
                  make_uint4(cnt[i][0], cnt[i][1], cnt[i][2], cnt[i][3]));
         if (s == 0) {  // segment 0: its aggregate is its inclusive prefix
 #pragma unroll
           for (int i = 0; i < kGroup; ++i)
-            __stcg(reinterpret_cast<uint4*>(incl + (int64_t)tile * ntile_vec + i * a.Wp + c0[k]),
+            __stcg(reinterpret_cast<uint4*>(incl + (int64_t)tile * ntile_vec + i * a.Wp + cl[k]),
                    make_uint4(cnt[i][0], cnt[i][1], cnt[i][2], cnt[i][3]));
         }
       }
@@ -480,7 +681,7 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
         for (int k = 0; k < CPL; ++k)
 #pragma unroll
           for (int i = 0; i < kGroup; ++i) {
-            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(src + i * a.Wp + c0[k]));
+            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(src + i * a.Wp + cl[k]));
             acc[k][0][i] += x.x;
             acc[k][1][i] += x.y;
             acc[k][2][i] += x.z;
@@ -496,8 +697,8 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
         for (int k = 0; k < CPL; ++k)
 #pragma unroll
           for (int i = 0; i < kGroup; ++i) {
-            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(own + i * a.Wp + c0[k]));
-            __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + c0[k]),
+            const uint4 x = __ldcg(reinterpret_cast<const uint4*>(own + i * a.Wp + cl[k]));
+            __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + cl[k]),
                    make_uint4(acc[k][0][i] + x.x, acc[k][1][i] + x.y, acc[k][2][i] + x.z,
                               acc[k][3][i] + x.w));
           }
@@ -532,9 +733,16 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
     }
     if (lane == 0) tot[0][0][warp] = make_uint4(run[0], run[1], run[2], run[3]);
     __syncthreads();
-    const uint4 t = lane < warp ? tot[0][0][lane] : make_uint4(0u, 0u, 0u, 0u);
-    const uint32_t wp[4] = {__reduce_add_sync(kFull, t.x), __reduce_add_sync(kFull, t.y),
-                            __reduce_add_sync(kFull, t.z), __reduce_add_sync(kFull, t.w)};
+    const uint4 tw = lane < warp ? tot[0][0][lane] : make_uint4(0u, 0u, 0u, 0u);
+    uint32_t wp[4] = {__reduce_add_sync(kFull, tw.x), __reduce_add_sync(kFull, tw.y),
+                      __reduce_add_sync(kFull, tw.z), __reduce_add_sync(kFull, tw.w)};
+    if (COLT && t > 0) {
+      const uint4 x = sls[0];
+      wp[0] += x.x;
+      wp[1] += x.y;
+      wp[2] += x.z;
+      wp[3] += x.w;
+    }
 #pragma unroll
     for (int k = 0; k < CPL; ++k)
 #pragma unroll
@@ -549,7 +757,7 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
   // plane; bin i is `i * plane_elems` further.  Stepped by W per row.
   uint32_t* prow[CPL];
 #pragma unroll
-  for (int k = 0; k < CPL; ++k) prow[k] = plane0 + rs * W + c0[k];
+  for (int k = 0; k < CPL; ++k) prow[k] = plane0 + rs * W + ct + cl[k];
   const bool full_group = nbins_here == kGroup;
   for (int b = nb_count; b < nb_total; ++b) {
     const int bi = b - nb_count;
@@ -586,13 +794,26 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
         tot[buf][rr][warp] = make_uint4(w4[0], w4[1], w4[2], w4[3]);
       }
     }
+    if (COLT && t > 0 && warp == 0 && lane < R) {
+      sleft[buf][lane] = lnext;
+      const int64_t rn = r0 + R + lane;
+      lnext = rn < re ? __ldg(reinterpret_cast<const uint4*>(lrow + rn * a.nbp))
+                      : make_uint4(0u, 0u, 0u, 0u);
+    }
     __syncthreads();  // totals visible; every warp is done reading the ring stage
     if (TMA && threadIdx.x == 0 && b + NST < nb_total) issue(b + NST);
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
-      const uint4 t = lane < warp ? tot[buf][rr][lane] : make_uint4(0u, 0u, 0u, 0u);
-      uint32_t run[kGroup] = {__reduce_add_sync(kFull, t.x), __reduce_add_sync(kFull, t.y),
-                              __reduce_add_sync(kFull, t.z), __reduce_add_sync(kFull, t.w)};
+      const uint4 tw = lane < warp ? tot[buf][rr][lane] : make_uint4(0u, 0u, 0u, 0u);
+      uint32_t run[kGroup] = {__reduce_add_sync(kFull, tw.x), __reduce_add_sync(kFull, tw.y),
+                              __reduce_add_sync(kFull, tw.z), __reduce_add_sync(kFull, tw.w)};
+      if (COLT && t > 0) {
+        const uint4 L = sleft[buf][rr];
+        run[0] += L.x;
+        run[1] += L.y;
+        run[2] += L.z;
+        run[3] += L.w;
+      }
       if (rr < rows) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
@@ -602,8 +823,7 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
             for (int i = 0; i < kGroup; ++i) acc[k][j][i] += run[i] + byte_of(v[rr][k][j], i);
 #pragma unroll
           for (int i = 0; i < kGroup; ++i) run[i] += byte_of(ct[rr][k], i);
-          const int c = c0[k];
-          if (c < W) {
+          if (colok[k]) {
             uint32_t* p = prow[k];
             if (VEC && full_group) {
 #pragma unroll
@@ -618,7 +838,7 @@ __global__ void __launch_bounds__(MAXT) k2_scan(ScanArgs a, RelLut lut) {
                   } else {
 #pragma unroll
                     for (int j = 0; j < 4; ++j)
-                      if (c + j < W) st_stream(p + j, acc[k][j][i]);
+                      if (!inval[k][j]) st_stream(p + j, acc[k][j][i]);
                   }
                 }
               }

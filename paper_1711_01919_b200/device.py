@@ -101,13 +101,13 @@ def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel
 
 
 PLAN_FIELDS = ("kernel", "launches", "segments", "segment_rows", "chunks_per_lane",
-               "rows_per_batch", "warps_per_cta", "workspace_bytes")
+               "rows_per_batch", "warps_per_cta", "workspace_bytes", "column_tiles", "tile_width")
 
 
 def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto",
          aligned16: bool = True) -> dict:
     """The launch plan the C ABI would use (ih_plan_describe); no device work."""
-    info = (ctypes.c_int64 * 8)()
+    info = (ctypes.c_int64 * len(PLAN_FIELDS))()
     _native.check(_native.lib().ih_plan_describe(frames, height, width, slab_bins,
                                                  _native.KERNELS[kernel], int(aligned16), info))
     d = dict(zip(PLAN_FIELDS, list(info)))

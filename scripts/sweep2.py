@@ -35,9 +35,12 @@ for spec in sys.argv[1:]:
         k, v = part.split("=")
         combos = [dict(c, **{k: x}) for c in combos for x in v.split(",")]
     for c in combos:
-        for k in ("IH_NSEG", "IH_TARGET_WARPS", "IH_ROWS_PER_BATCH", "IH_MIN_SEG_ROWS", "IH_NO_TMA", "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX"):
+        for k in ("IH_NSEG", "IH_TARGET_WARPS", "IH_ROWS_PER_BATCH", "IH_MIN_SEG_ROWS", "IH_NO_TMA", "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE"):
             os.environ.pop(k, None)
         os.environ.update(c)
         prep, scan, tot, frac, sfrac = timed(name)
-        print(json.dumps({"wl": name, **c, "prep_ms": round(prep, 4), "scan_ms": round(scan, 4),
+        import subprocess
+        clk = subprocess.run(["nvidia-smi", "--query-gpu=clocks.sm,clocks_throttle_reasons.active,temperature.gpu,power.draw",
+                              "--format=csv,noheader"], capture_output=True, text=True).stdout.strip()
+        print(json.dumps({"wl": name, **c, "clk": clk, "prep_ms": round(prep, 4), "scan_ms": round(scan, 4),
                           "total_ms": round(tot, 4), "frac_total": round(frac, 3), "frac_scan": round(sfrac, 3)}), flush=True)

@@ -72,6 +72,7 @@ def test_validation_order_without_device():
     assert _call(H=1 << 16, W=(1 << 16) + 1, pitch=0) == _native.IH_ERR_CAPACITY
     assert _call(pitch=3) == _native.IH_ERR_PARAM
     assert _call(kernel=7) == _native.IH_ERR_PARAM
+    # column-tiled single pass: the row carries need a workspace
     assert _call(W=20000, pitch=20000, kernel=_native.KERNEL_SINGLE_PASS) == _native.IH_ERR_PARAM
 
 
@@ -101,6 +102,24 @@ def test_workspace_plan():
         assert n > 0 and n % (frames * 32 * 1920 * 2) == 0
     # tiny problems with few rows need no carries
     assert L.ih_workspace_bytes(1, 20, 64, 4, 0) == 0
-    # cross-weave needs none; too-wide images fall back to cross-weave under auto
+    # cross-weave needs none
     assert L.ih_workspace_bytes(1, 1080, 1920, 32, _native.KERNEL_CROSSWEAVE) == 0
-    assert L.ih_workspace_bytes(1, 16, 20000, 8, 0) == 0
+    # column tiles (W > 2048): k2_rowleft's (T-1, H, nbp) u32 row carries; 20000
+    # columns -> 10 tiles of 2048 (16 chunks) ... as even as possible
+    n = L.ih_workspace_bytes(1, 16, 20000, 8, 0)
+    assert n >= 9 * 16 * 8 * 4
+
+
+def test_column_tile_plan():
+    """W > 2048 splits rows into column tiles of <= 16 chunks, as even as possible."""
+    from paper_1711_01919_b200 import device
+
+    p = device.plan(1, 2160, 3840, 128)
+    assert (p["kernel"], p["column_tiles"], p["tile_width"], p["chunks_per_lane"]) == \
+        ("single_pass", 2, 1920, 1)
+    p = device.plan(1, 8192, 8192, 32)
+    assert (p["column_tiles"], p["tile_width"]) == (4, 2048)
+    p = device.plan(64, 1080, 1920, 32)
+    assert (p["column_tiles"], p["tile_width"]) == (1, 1920)
+    p = device.plan(1, 3, 30001, 4)
+    assert p["column_tiles"] * p["tile_width"] >= 30001 and p["tile_width"] <= 2048

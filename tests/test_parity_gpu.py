@@ -26,7 +26,7 @@ def crc_of(t) -> str:
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
     for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
-              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX"):
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -60,8 +60,6 @@ def test_c7_worker_caps_do_not_change_output(golden_c1):
 def test_small_cases_exact(golden_small, kernel):
     for name, case in golden_small.items():
         px, lut, bins = case["img"], case["lut"], int(case["bins"])
-        if kernel == "single_pass" and px.shape[1] > 8192:
-            continue
         got = dev_compute(px, lut, bins, kernel=kernel).cpu().numpy()
         assert np.array_equal(got, case["counts"]), (name, kernel)
 
@@ -195,11 +193,79 @@ def test_frames_batch(rng):
         assert np.array_equal(t[f].cpu().numpy(), O.compute_crossweave(frames[f], lut, 9))
 
 
-def test_wide_image_falls_back_to_crossweave(rng):
+def test_wide_image_without_column_tiles_falls_back_to_crossweave(monkeypatch, rng):
+    monkeypatch.setenv("IH_NO_COLTILE", "1")
+    assert device.plan(1, 3, 10000, 6)["kernel"] == "crossweave"
     px = rng.integers(0, 256, (3, 10000), dtype=np.uint8)
     lut = O.np_uniform_table(6)
     got = dev_compute(px, lut, 6).cpu().numpy()
     assert np.array_equal(got, O.compute_crossweave(px, lut, 6))
+
+
+COLT_SHAPES = [(1, 2049), (3, 2177), (33, 4100), (70, 3840), (20, 8192), (9, 10000),
+               (130, 6001), (2, 30001)]
+
+
+@pytest.mark.parametrize("nseg", [0, 1, 3, 30])
+@pytest.mark.parametrize("tma", [True, False])
+@pytest.mark.parametrize("rows_per_batch", [1, 4])
+def test_column_tiles(monkeypatch, rng, nseg, tma, rows_per_batch):
+    """Column-tiled K2 (W > 2048): k2_rowleft row carries + the carry table summed
+    left of each tile, with and without row segments, TMA and LDG inputs,
+    ragged last tiles, every width up to 30001 through the single pass."""
+    if nseg:
+        monkeypatch.setenv("IH_NSEG", str(nseg))
+    if not tma:
+        monkeypatch.setenv("IH_NO_TMA", "1")
+    monkeypatch.setenv("IH_ROWS_PER_BATCH", str(rows_per_batch))
+    for (h, w) in COLT_SHAPES:
+        bins = int(rng.choice([1, 4, 7, 32, 256]))
+        px = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        lut = O.np_uniform_table(bins)
+        p = device.plan(1, h, w, bins)
+        assert p["kernel"] == "single_pass", (h, w)
+        got = dev_compute(px, lut, bins, kernel="single_pass").cpu().numpy()
+        assert np.array_equal(got, O.compute_crossweave(px, lut, bins)), (h, w, bins)
+
+
+@pytest.mark.parametrize("slab_counts", [False, True])
+def test_colcounts_variants_256_bins(monkeypatch, rng, slab_counts):
+    """Carry tables from k2_colcounts_all (one pass, shared atomics, all bins)
+    and from the per-32-bin-slab k2_colcounts; 256 bins, explicit LUTs, bin
+    slabs whose padding takes the out-of-slab marker."""
+    if slab_counts:
+        monkeypatch.setenv("IH_COLCOUNTS_SLAB", "1")
+    monkeypatch.setenv("IH_NSEG", "5")
+    for (h, w) in [(300, 1000), (97, 2500), (64, 130)]:
+        px = rng.integers(0, 256, (h, w), dtype=np.uint8)
+        for bins, rng_ in [(256, None), (256, (3, 256)), (100, (0, 99)), (33, (1, 33))]:
+            lut = O.np_uniform_table(bins) if bins == 256 else rng.integers(0, bins, 256).astype(np.uint8)
+            full = O.compute_crossweave(px, lut, bins)
+            got = dev_compute(px, lut, bins, kernel="single_pass", bin_range=rng_).cpu().numpy()
+            lo, hi = rng_ or (0, bins)
+            assert np.array_equal(got, full[lo:hi]), (h, w, bins, rng_)
+
+
+def test_column_tiles_unaligned_slabs_and_frames(rng):
+    """Column tiles with an odd pitch / byte offset (LDG rows), bin slabs and a
+    frame batch; constant columns stress the row-carry atomics."""
+    h, w, bins = 41, 5003, 37
+    base = rng.integers(0, 256, (h, w + 5), dtype=np.uint8)
+    base[:, :900] = 200  # one bin hit by every pixel of the left tile
+    px = np.ascontiguousarray(base[:, 1:1 + w])
+    lut = O.np_uniform_table(bins)
+    full = O.compute_crossweave(px, lut, bins)
+    view = torch.from_numpy(base).cuda()[:, 1:1 + w]
+    got = device.integral_histogram(view, lut, bins, kernel="single_pass").cpu().numpy()
+    assert np.array_equal(got, full)
+    from paper_1711_01919_b200 import sharding
+    for lo, hi in sharding.bin_slabs(bins, 4):
+        got = dev_compute(px, lut, bins, kernel="single_pass", bin_range=(lo, hi))
+        assert np.array_equal(got.cpu().numpy(), full[lo:hi]), (lo, hi)
+    frames = rng.integers(0, 256, (3, 50, 4500), dtype=np.uint8)
+    t = ih.compute_frames(frames, ih.BinSpec.uniform(9))
+    for f in range(3):
+        assert np.array_equal(t[f].cpu().numpy(), O.compute_crossweave(frames[f], O.np_uniform_table(9), 9))
 
 
 # ------------------------------------------------------- BASELINE configs (golden)
@@ -355,7 +421,7 @@ def test_plan_describe_matches_launches():
     p = device.plan(64, 1080, 1920, 32)
     assert p["kernel"] == "single_pass" and p["launches"] in (1, 2, 3)
     assert p["segments"] * p["segment_rows"] >= 1080
-    assert device.plan(1, 4, 20000, 8)["kernel"] == "crossweave"
+    assert device.plan(1, 4, 20000, 8)["kernel"] == "single_pass"  # column tiles
     assert device.workspace_bytes(64, 1080, 1920, 32) >= p["workspace_bytes"]
 
 
