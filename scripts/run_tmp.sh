@@ -1,6 +1,7 @@
-mkdir -p gpurun_out
-timeout 900 python -m pytest tests/ -q -x -m gpu > gpurun_out/pytest_ct6.log 2>&1; echo pytest=$?
-timeout 900 python scripts/sweep2.py 'hd64' 'hd32' 'hd16' 'hd8' 'hd1' '512' '4k128' '4k128/2' '4k128/4' '4k128/8' '8k256/8' '8k256' > gpurun_out/sweep_ct6.jsonl 2>&1; echo sweep=$?
-timeout 600 python bench.py > gpurun_out/bench_ct6_hd64.json 2> gpurun_out/bench_ct6_hd64.err; echo bench=$?
-timeout 600 python bench.py --workload 4k128 > gpurun_out/bench_ct6_4k128.json 2> gpurun_out/bench_ct6_4k128.err; echo bench4k=$?
-timeout 900 python bench.py --workload 8k256 > gpurun_out/bench_ct6_8k256.json 2> gpurun_out/bench_ct6_8k256.err; echo bench8k=$?
+mkdir -p gpurun_out/san
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool python scripts/sanitize_cases.py > gpurun_out/san/$tool.txt 2>&1; echo $tool=$?
+done
+timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01e_8k256.csv python bench.py --workload 8k256 --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1; echo l8k=$?
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:"k2_scan|k2_rowleft|k2_colcounts_all" -c 3 -o gpurun_out/prof_8k256 -f python scripts/one.py 8k256 > /dev/null 2>&1; echo ncu8k=$?
+timeout 400 ncu --set full --clock-control none --import-source on -k regex:"k2_scan|k2_colcounts_all" -c 2 -o gpurun_out/prof_hd64 -f python scripts/one.py hd64 > /dev/null 2>&1; echo ncuhd=$?

@@ -1,4 +1,5 @@
 """Small parity cases for compute-sanitizer: every K2 carry mode / input path,
+column tiles (k2_rowleft), both count-table kernels,
 K1/K1b, K3, K4, K5 -- each checked against the oracle."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -7,13 +8,16 @@ from oracle import oracle as O
 from paper_1711_01919_b200 import device
 
 rng = np.random.default_rng(7)
-cases = [(1, 1, 3), (7, 131, 5), (61, 257, 16), (100, 300, 64), (33, 2049, 7), (40, 4100, 9), (9, 8192, 4)]
+cases = [(1, 1, 3), (7, 131, 5), (61, 257, 16), (100, 300, 64), (33, 2049, 7), (40, 4100, 9), (9, 8192, 4),
+         (21, 10001, 256), (70, 3840, 128)]
 envs = [{}, {"IH_NSEG": "3"}, {"IH_NSEG": "5", "IH_TABLE_SUM_MAX": "1"},
         {"IH_NSEG": "4", "IH_CARRY_LOOKBACK": "1"}, {"IH_NO_TMA": "1", "IH_NSEG": "2"},
-        {"IH_ROWS_PER_BATCH": "1", "IH_NSEG": "3"}]
+        {"IH_ROWS_PER_BATCH": "1", "IH_NSEG": "3"}, {"IH_NSEG": "6", "IH_COLCOUNTS_SLAB": "1"},
+        {"IH_NSEG": "3", "IH_NO_COLTILE": "1"}]
 bad = 0
 for env in envs:
-    for k in ("IH_NSEG", "IH_TABLE_SUM_MAX", "IH_CARRY_LOOKBACK", "IH_NO_TMA", "IH_ROWS_PER_BATCH"):
+    for k in ("IH_NSEG", "IH_TABLE_SUM_MAX", "IH_CARRY_LOOKBACK", "IH_NO_TMA", "IH_ROWS_PER_BATCH",
+              "IH_COLCOUNTS_SLAB", "IH_NO_COLTILE"):
         os.environ.pop(k, None)
     os.environ.update(env)
     for (h, w, b) in cases:
@@ -21,6 +25,8 @@ for env in envs:
         lut = O.np_uniform_table(b)
         want = O.compute_crossweave(px, lut, b)
         for kernel in ("auto", "crossweave"):
+            if kernel == "crossweave" and w > 8192:
+                continue
             got = device.integral_histogram(device.upload_image(px), lut, b, kernel=kernel).cpu().numpy()
             if not np.array_equal(got, want):
                 bad += 1; print("MISMATCH", env, h, w, b, kernel)
