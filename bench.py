@@ -97,11 +97,9 @@ def measured_peaks():
 def committed_traffic(wl: Workload):
     """dram__bytes_read.sum + dram__bytes_write.sum per histogram of k2_scan from
     the committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
-    if wl.key != "hd64":
-        return None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            return json.load(fh).get("k2_scan_hd_bytes_per_frame")
+            return json.load(fh)["per_histogram"][wl.key]["bytes"]
     except Exception:
         return None
 
@@ -391,7 +389,7 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
         "hbm_frac_step": value * wl.alg_bytes / 1e9 / peak / world,
         "roofline": {"bound": "hbm", "kernel": "k2_scan", "achieved": achieved, "peak": peak,
                      "peak_source": peak_src, "unit": "GB/s", "frac": achieved / peak,
-                     "traffic": (traffic * nloc if traffic else None),
+                     "traffic": (traffic * nloc if traffic and nb == wl.bins else None),
                      "alg_bytes_per_launch": alg_launch, "launch_ms": scan_ms,
                      "prepare_exposed_ms": prep_ms, "rank0_share": [f0, f1, b0, b1]},
         "pipelined_steps": bool(args.overlap),

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <utility>
 
 #include "../../include/inthist_b200.h"
 #include "ih_kernels.cuh"
@@ -34,6 +35,25 @@ int64_t env_int(const char* name, int64_t dflt) {
 }
 
 constexpr int kNumSMs = 148;
+
+// Launch with programmatic stream serialization when `pdl` (see ih_kernels.cuh
+// griddep_wait): only for a kernel whose stream predecessor is a kernel this
+// same call launched, so user work before the call is always fully ordered.
+template <typename... KArgs, typename... Args>
+cudaError_t launch(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                   bool pdl, Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------------ planning
 struct K2Plan {
@@ -124,11 +144,13 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   p.vec = vec;
   p.tma = tma;
   const int64_t nchunks = (W + ih::kChunk - 1) / ih::kChunk;
-  if (nchunks > 16 && env_int("IH_NO_COLTILE", 0) == 0) {
+  int64_t tile_chunks = env_int("IH_TILE_CHUNKS", 16);  // max chunks per column tile
+  if (tile_chunks < 1 || tile_chunks > 16) tile_chunks = 16;
+  if (nchunks > tile_chunks && env_int("IH_NO_COLTILE", 0) == 0) {
     // W > 2048: column tiles of <= 16 chunks (CPL 1), as even as possible
     p.colt = true;
     p.cpl = 1;
-    p.T = (int)((nchunks + 15) / 16);
+    p.T = (int)((nchunks + tile_chunks - 1) / tile_chunks);
   } else if (vec && tma && env_int("IH_NO_BIG", 0) == 0 && nchunks > 16 && nchunks <= 32) {
     // W in (2048, 4096]: one 1024-thread CTA per SM, CPL 1 at <= 64 registers
     p.big = true;
@@ -234,7 +256,7 @@ size_t lb_header_bytes(int64_t frames, const K2Plan& p) {
   return 16 + (size_t)((lb_tiles(frames, p) * 4 + 15) / 16 * 16);
 }
 //   column tiles:   [CARRY_TABLE table, 256 B aligned][rowleft: (frames, T-1, H, nbp) u32]
-//                   [segleft: (frames, nseg, T-1, nbp) u32, when nseg > 1]
+//                   [chunktot: (frames, nseg, Wp/128, nbp) u32 per-chunk table totals, nseg > 1]
 size_t k2_table_bytes(int64_t frames, const K2Plan& p) {
   if (p.carry != ih::CARRY_TABLE) return 0;
   return ((size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint16_t) + 255) / 256 * 256;
@@ -243,13 +265,13 @@ size_t k2_rowleft_bytes(int64_t frames, int64_t H, const K2Plan& p) {
   if (!p.colt || p.T < 2) return 0;
   return (size_t)frames * (p.T - 1) * H * p.nbp * sizeof(uint32_t);
 }
-size_t k2_segleft_bytes(int64_t frames, const K2Plan& p) {
-  if (!p.colt || p.T < 2 || p.nseg < 2) return 0;
-  return (size_t)frames * p.nseg * (p.T - 1) * p.nbp * sizeof(uint32_t);
+size_t k2_chunktot_bytes(int64_t frames, const K2Plan& p) {
+  if (!p.colt || p.T < 2 || p.carry != ih::CARRY_TABLE) return 0;
+  return (size_t)frames * p.nseg * (p.Wp / ih::kChunk) * p.nbp * sizeof(uint32_t);
 }
 size_t k2_ws_bytes(int64_t frames, int64_t H, const K2Plan& p) {
   if (p.colt)
-    return k2_table_bytes(frames, p) + k2_rowleft_bytes(frames, H, p) + k2_segleft_bytes(frames, p);
+    return k2_table_bytes(frames, p) + k2_rowleft_bytes(frames, H, p) + k2_chunktot_bytes(frames, p);
   if (p.carry == ih::CARRY_TABLE) return (size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint16_t);
   if (p.carry == ih::CARRY_LOOKBACK)
     return lb_header_bytes(frames, p) +
@@ -265,6 +287,9 @@ struct Call {
   int kernel;
   K2Plan plan;
   cudaStream_t stream;
+  mutable int launched = 0;  // kernels this call has launched (PDL eligibility)
+  bool pdl_ok = false;       // PDL allowed (IH_NO_PDL unset)
+  bool pdl() const { return pdl_ok && launched > 0; }
 };
 
 // Validation in the reference's order: shape (core.py:28-36, :72-79),
@@ -288,6 +313,7 @@ ih_status validate(const uint8_t* img, int64_t frames, int64_t H, int64_t W, int
   if (kernel < IH_KERNEL_AUTO || kernel > IH_KERNEL_CROSSWEAVE)
     return fail(IH_ERR_PARAM, "unknown kernel");
   c->img = img;
+  c->pdl_ok = env_int("IH_NO_PDL", 0) == 0;
   c->frames = frames;
   c->H = H;
   c->W = W;
@@ -323,22 +349,14 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
   if (need == 0) return IH_OK;
   if (ws_bytes < need || !ws)
     return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
-  if (p.colt && p.T > 1) {  // row counts left of each tile boundary (+ per-segment sums)
+  if (p.colt && p.T > 1) {  // row counts left of each tile boundary
     uint32_t* lc = (uint32_t*)((uint8_t*)ws + k2_table_bytes(c.frames, p));
-    uint32_t* sl = nullptr;
-    if (k2_segleft_bytes(c.frames, p)) {
-      sl = (uint32_t*)((uint8_t*)lc + k2_rowleft_bytes(c.frames, c.H, p));
-      if (cudaMemsetAsync(sl, 0, k2_segleft_bytes(c.frames, p), c.stream) != cudaSuccess)
-        return cuda_fail("segleft reset");
-    }
     dim3 grid((unsigned)((c.H + ih::kRowLeftWarps - 1) / ih::kRowLeftWarps), (unsigned)c.frames);
-    if (aligned_rows(c))
-      ih::k2_rowleft<true><<<grid, ih::kRowLeftWarps * 32, 0, c.stream>>>(
-          c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.nbp, p.T, p.TW, p.S, p.nseg, lc, sl);
-    else
-      ih::k2_rowleft<false><<<grid, ih::kRowLeftWarps * 32, 0, c.stream>>>(
-          c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.nbp, p.T, p.TW, p.S, p.nseg, lc, sl);
-    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_rowleft");
+    if (launch(aligned_rows(c) ? ih::k2_rowleft<true> : ih::k2_rowleft<false>, grid,
+               dim3(ih::kRowLeftWarps * 32), 0, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
+               c.fstride, c.lut, p.nbp, p.T, p.TW, lc) != cudaSuccess)
+      return cuda_fail("k2_rowleft");
+    ++c.launched;
   }
   if (p.carry == ih::CARRY_NONE) return IH_OK;
   if (p.carry == ih::CARRY_LOOKBACK) {  // reset the ticket and the tile flags
@@ -347,6 +365,10 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
     return IH_OK;
   }
   const bool al = aligned_rows(c);
+  uint32_t* ctot = k2_chunktot_bytes(c.frames, p)
+                       ? (uint32_t*)((uint8_t*)ws + k2_table_bytes(c.frames, p) +
+                                     k2_rowleft_bytes(c.frames, c.H, p))
+                       : nullptr;
   if (env_int("IH_COLCOUNTS_SLAB", 0) == 0) {  // all bins in one pass (shared atomics)
     dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
     auto kern = al ? ih::k2_colcounts_all<true> : ih::k2_colcounts_all<false>;
@@ -355,9 +377,10 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
             cudaSuccess)
       return cuda_fail("k2_colcounts_all smem attribute");
-    kern<<<grid, 256, smem, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S, p.nseg,
-                                        p.nbp, p.Wp, (uint16_t*)ws);
-    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts_all");
+    if (launch(kern, grid, dim3(256), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
+               c.fstride, c.lut, p.S, p.nseg, p.nbp, p.Wp, (uint16_t*)ws, ctot) != cudaSuccess)
+      return cuda_fail("k2_colcounts_all");
+    ++c.launched;
     return launch_colprefix(c, ws);
   }
   const int nslab = (p.nbp + ih::kCountSlab - 1) / ih::kCountSlab;
@@ -373,9 +396,10 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
     return cuda_fail("k2_colcounts smem attribute");
-  kern<<<grid, nw * 32, smem, c.stream>>>(c.img, c.H, c.W, c.pitch, c.fstride, c.lut, p.S, p.nseg,
-                                          p.nbp, p.Wp, nslab, (uint16_t*)ws);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colcounts");
+  if (launch(kern, grid, dim3(nw * 32), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
+             c.fstride, c.lut, p.S, p.nseg, p.nbp, p.Wp, nslab, (uint16_t*)ws, ctot) != cudaSuccess)
+    return cuda_fail("k2_colcounts");
+  ++c.launched;
   return launch_colprefix(c, ws);
 }
 
@@ -385,9 +409,10 @@ ih_status launch_colprefix(const Call& c, void* ws) {
   const int64_t total = c.frames * p.nbp * p.Wp / 4 * ih::kPrefixLanes;  // 8 lanes per quad
   int64_t blocks = (total + 255) / 256;
   if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
-  ih::k2_colprefix<<<(unsigned)blocks, 256, 0, c.stream>>>((uint16_t*)ws, c.frames, p.nseg, p.nbp,
-                                                           p.Wp);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_colprefix");
+  if (launch(ih::k2_colprefix, dim3((unsigned)blocks), dim3(256), 0, c.stream, c.pdl(),
+             (uint16_t*)ws, c.frames, p.nseg, p.nbp, p.Wp) != cudaSuccess)
+    return cuda_fail("k2_colprefix");
+  ++c.launched;
   return IH_OK;
 }
 
@@ -399,8 +424,11 @@ ih_status launch_k2(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads
       cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess)
     return cuda_fail("k2_scan smem attribute");
-  fn<<<grid, threads, smem, c.stream>>>(a, c.lut);
-  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k2_scan");
+  // look-back carries read flags a memset just reset: never PDL there
+  const bool pdl = c.pdl() && c.plan.carry != ih::CARRY_LOOKBACK;
+  if (launch(fn, grid, dim3(threads), smem, c.stream, pdl, a, c.lut) != cudaSuccess)
+    return cuda_fail("k2_scan");
+  ++c.launched;
   return IH_OK;
 }
 
@@ -446,9 +474,9 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
   a.row_bytes = (uint32_t)((c.W + 15) / 16 * 16);
   a.rowleft = p.colt && p.T > 1 ? (const uint32_t*)((const uint8_t*)ws + k2_table_bytes(c.frames, p))
                                 : nullptr;
-  a.segleft = k2_segleft_bytes(c.frames, p)
-                  ? (const uint32_t*)((const uint8_t*)a.rowleft + k2_rowleft_bytes(c.frames, c.H, p))
-                  : nullptr;
+  a.chunktot = k2_chunktot_bytes(c.frames, p)
+                   ? (const uint32_t*)((const uint8_t*)a.rowleft + k2_rowleft_bytes(c.frames, c.H, p))
+                   : nullptr;
   a.colpre = p.carry == ih::CARRY_TABLE ? (const uint16_t*)ws : nullptr;
   a.table_is_prefix = table_prefix_h(p, c.H) ? 1 : 0;
   a.lb_ticket = a.lb_flags = a.lb_agg = a.lb_incl = nullptr;

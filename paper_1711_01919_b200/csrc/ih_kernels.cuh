@@ -41,6 +41,19 @@ __device__ __forceinline__ uint32_t warp_incl_scan(uint32_t x, int lane) {
   return x;
 }
 
+// Programmatic dependent launch (PDL).  A kernel launched with programmatic
+// stream serialization may start while its predecessor in the stream still
+// runs; griddep_wait() blocks until that predecessor has completed and its
+// writes are visible (a no-op without the launch attribute).  Kernels of the
+// prepare chain call griddep_launch_dependents() once they are running so the
+// next kernel's prologue (TMA ring fill, one-hot table) overlaps their tail.
+// Every PDL-launched kernel waits before it completes, so completion stays
+// transitive along the chain.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch_dependents() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 // Streaming (evict-first) 16-byte / 4-byte global stores: every output byte
 // is written exactly once and never re-read by the producing kernel.
 __device__ __forceinline__ void st_stream_v4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c,

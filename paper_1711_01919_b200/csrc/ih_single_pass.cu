@@ -46,7 +46,8 @@ constexpr size_t kCountWarpSmem = (size_t)kCountRows * 4 * 32 * sizeof(uint16_t)
 template <bool ALIGNED, int kCountWarps>
 __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
-    RelLut lut, int S, int nseg, int nbp, int64_t Wp, int nslab, uint16_t* __restrict__ ws) {
+    RelLut lut, int S, int nseg, int nbp, int64_t Wp, int nslab, uint16_t* __restrict__ ws,
+    uint32_t* __restrict__ ctot) {
   extern __shared__ __align__(16) uint16_t chist[];  // [warp][bin row][k][lane]
   __shared__ uint16_t sofs[512];  // pixel -> byte offset of its bin row (dummy row if none)
   const int lane = threadIdx.x & 31;
@@ -57,6 +58,7 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
   const int64_t f = blockIdx.z / nslab;
   const uint32_t lo = (uint32_t)slab * kCountSlab;
   constexpr uint32_t kRowBytes = 4 * 32 * sizeof(uint16_t);  // one bin row: [k][lane]
+  griddep_launch_dependents();
   for (int v = threadIdx.x; v < 512; v += blockDim.x) {
     const uint32_t d = v < 256 ? (uint32_t)lut.rel[v] - lo : 0xffffffffu;
     sofs[v] = (uint16_t)((d < (uint32_t)kCountSlab ? d : (uint32_t)kCountSlab) * kRowBytes);
@@ -112,6 +114,7 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
     }
   }
   __syncthreads();
+  griddep_wait();  // PDL: complete only after the predecessor (transitivity)
   // sum the 8 private histograms; item = (bin, lane) -> 4 columns, one 8-byte store
   const int nbs = min(kCountSlab, nbp - (int)lo);
   uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp + lo) * Wp + (int64_t)blockIdx.x * kChunk;
@@ -125,6 +128,10 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
         sum[k] += chist[(size_t)w * kCountRows * 4 * 32 + (b * 4 + k) * 32 + l];
     *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) =
         make_uint2(sum[0] | (sum[1] << 16), sum[2] | (sum[3] << 16));
+    if (ctot) {  // column-tiled scans: the chunk's total per bin (warp-uniform b)
+      const uint32_t t = __reduce_add_sync(kFull, sum[0] + sum[1] + sum[2] + sum[3]);
+      if (l == 0) ctot[((f * nseg + s) * (int64_t)gridDim.x + blockIdx.x) * nbp + lo + b] = t;
+    }
   }
 }
 
@@ -142,7 +149,8 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
 template <bool ALIGNED>
 __global__ void __launch_bounds__(256) k2_colcounts_all(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
-    RelLut lut, int S, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws) {
+    RelLut lut, int S, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws,
+    uint32_t* __restrict__ ctot) {
   extern __shared__ __align__(16) uint32_t hist2[];  // [nbp][2][32]
   __shared__ uint32_t sw[512];  // pixel (| 256 past the edge) -> word offset of its bin, or ~0
   const int lane = threadIdx.x & 31;
@@ -151,6 +159,7 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
   const int64_t c = (int64_t)blockIdx.x * kChunk + 4 * lane;
   const int s = blockIdx.y;
   const int64_t f = blockIdx.z;
+  griddep_launch_dependents();
   for (int v = threadIdx.x; v < 512; v += blockDim.x) {
     const uint32_t b = v < 256 ? (uint32_t)lut.rel[v] : 0xffffffffu;
     sw[v] = b < (uint32_t)nbp ? b * 64u : 0xffffffffu;
@@ -197,11 +206,17 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
     }
   }
   __syncthreads();
+  griddep_wait();  // PDL: complete only after the predecessor (transitivity)
   uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp) * Wp + (int64_t)blockIdx.x * kChunk;
-  for (int e = threadIdx.x; e < nbp * 32; e += blockDim.x) {
+  uint32_t* tdst = ctot ? ctot + ((f * nseg + s) * (int64_t)gridDim.x + blockIdx.x) * nbp : nullptr;
+  for (int e = threadIdx.x; e < nbp * 32; e += blockDim.x) {  // warp-uniform bin b
     const int l = e & 31, b = e >> 5;
-    *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) =
-        make_uint2(hist2[(b * 2) * 32 + l], hist2[(b * 2 + 1) * 32 + l]);
+    const uint32_t w0 = hist2[(b * 2) * 32 + l], w1 = hist2[(b * 2 + 1) * 32 + l];
+    *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) = make_uint2(w0, w1);
+    if (tdst) {  // column-tiled scans: the chunk's total per bin
+      const uint32_t sum = __reduce_add_sync(kFull, (w0 & 0xffffu) + (w0 >> 16) + (w1 & 0xffffu) + (w1 >> 16));
+      if (l == 0) tdst[b] = sum;
+    }
   }
 }
 
@@ -228,6 +243,8 @@ __global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, i
   const int sub = threadIdx.x & (kPrefixLanes - 1);
   const int per = (nseg + kPrefixLanes - 1) / kPrefixLanes;  // slots per lane
   const int j0 = sub * per, j1 = min(nseg, j0 + per);
+  griddep_launch_dependents();
+  griddep_wait();  // PDL: the count table is complete
   for (int64_t gi = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / kPrefixLanes; ;
        gi += (int64_t)gridDim.x * blockDim.x / kPrefixLanes) {
     // all 8 lanes of a group iterate together (the shuffles need them)
@@ -260,10 +277,7 @@ __global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, i
 // ---------------------------------------------------------------------------
 // k2_rowleft: column-tile row carries for the COLT scan.
 //   lc[f][t][r][b] = #{ c < (t+1)*TW : Q(I(r,c)) = b },  t < T-1, b < nbp  (u32)
-// i.e. H_b restricted to row r at the last column left of tile t+1, and
-//   sl[f][s][t][b] += lc[f][t][r][b] over the rows r of segment s < nseg-1
-// (zeroed by the host first) -- the part of the segment carry H_b(r_s-1, .)
-// left of a tile.  Warp per row walking the row left to right (one 32-bit
+// i.e. H_b restricted to row r at the last column left of tile t+1.  Warp per row walking the row left to right (one 32-bit
 // pixel load per lane per 128-column chunk, 16 chunks of loads in flight)
 // into a warp-private shared histogram; the histogram is cumulative, so at
 // each tile boundary it is dumped as is (coalesced, one u32 per bin).
@@ -273,12 +287,12 @@ constexpr int kRowLeftWarps = 8;
 template <bool ALIGNED>
 __global__ void __launch_bounds__(kRowLeftWarps * 32) k2_rowleft(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
-    RelLut lut, int nbp, int T, int TW, int S, int nseg, uint32_t* __restrict__ lc,
-    uint32_t* __restrict__ sl) {
+    RelLut lut, int nbp, int T, int TW, uint32_t* __restrict__ lc) {
   __shared__ uint32_t hist[kRowLeftWarps][256];
   __shared__ uint8_t rel[256];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
+  griddep_launch_dependents();
   for (int v = threadIdx.x; v < 256; v += blockDim.x) rel[v] = lut.rel[v];
   for (int v = lane; v < 256; v += 32) hist[warp][v] = 0u;
   __syncthreads();
@@ -305,8 +319,6 @@ __global__ void __launch_bounds__(kRowLeftWarps * 32) k2_rowleft(
     }
   };
   const int cpt = TW / kChunk;  // chunks per tile
-  const int64_t s = r / S;
-  const bool seg_sum = sl != nullptr && s + 1 < nseg;
   constexpr int U = 16;
   for (int t = 0; t + 1 < T; ++t) {
     const int64_t cb = (int64_t)t * TW + 4 * lane;
@@ -320,12 +332,7 @@ __global__ void __launch_bounds__(kRowLeftWarps * 32) k2_rowleft(
     }
     __syncwarp();
     uint32_t* dst = lc + (((f * (T - 1) + t) * H) + r) * (int64_t)nbp;
-    uint32_t* sdst = sl + ((f * nseg + s) * (T - 1) + t) * (int64_t)nbp;
-    for (int b = lane; b < nbp; b += 32) {
-      const uint32_t v = h[b];
-      dst[b] = v;
-      if (seg_sum && v) atomicAdd(sdst + b, v);
-    }
+    for (int b = lane; b < nbp; b += 32) dst[b] = h[b];
     __syncwarp();
   }
 }
@@ -340,7 +347,7 @@ __global__ void __launch_bounds__(kRowLeftWarps * 32) k2_rowleft(
 //        ahead of the consumers; otherwise lanes load pixels with LDG.
 //   COLT column tiles: the CTA covers columns [t*TW, (t+1)*TW) of the row;
 //        rows get the counts left of the tile from k2_rowleft, the segment
-//        carry adds k2_rowleft's per-segment sums of those over the segments above.
+//        carry adds the count kernel's chunk totals left of the tile, segments above.
 // ---------------------------------------------------------------------------
 struct ScanArgs {
   const uint8_t* img;
@@ -353,7 +360,7 @@ struct ScanArgs {
   int TW;          // tile width = warps * CPL * 128 = row stride of the smem ring
   uint32_t row_bytes;      // bytes copied per row by TMA = round_up(W, 16) (T == 1)
   const uint32_t* rowleft; // COLT: (frames, T-1, H, nbp) u32 row counts left of tile t+1
-  const uint32_t* segleft; // COLT: (frames, nseg, T-1, nbp) u32 their sums per segment
+  const uint32_t* chunktot; // COLT: (frames, nseg, Wp/128, nbp) u32 per-chunk totals of the count table
   const uint16_t* colpre;  // CARRY_TABLE: (frames, nseg, nbp, Wp) u16 column counts or prefixes
   int table_is_prefix;     // 1: slot s holds sum_{s'<s} counts (k2_colprefix ran); 0: raw counts
   uint32_t* lb_ticket;     // CARRY_LOOKBACK: tile ticket counter (zeroed per launch)
@@ -435,7 +442,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   __shared__ uint32_t oh[kOneHotEntries];
   __shared__ uint4 tot[2][R][32];
   __shared__ uint4 sleft[2][COLT ? R : 1];  // COLT: per-row counts left of the tile
-  __shared__ uint4 sls[1];                  // COLT: carry part left of the tile
+  __shared__ uint4 sls[COLT ? 32 : 1];      // COLT: per-warp carry parts left of the tile
   __shared__ __align__(8) uint64_t full_bar[NST];
   __shared__ uint32_t s_tile, s_flag;
   extern __shared__ __align__(128) uint8_t ring[];  // [NST][R][Wp] image rows (TMA)
@@ -509,6 +516,10 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     for (int j = 0; j < 4; ++j) inval[k][j] = (ct + cl[k] + j < W) ? 0u : 256u;
   }
 
+  // PDL: everything above touches only the image (never written by the
+  // prepare kernels) and shared memory; the carry tables are read below
+  griddep_wait();
+
   // output: bin i of this group at plane0 + i * plane_stride (bins >= nb masked)
   const int64_t plane_elems = H * W;
   bool colok[CPL];
@@ -530,6 +541,27 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   if (CARRY == CARRY_TABLE && s > 0) {
     const int64_t plane_sz = (int64_t)a.nbp * a.Wp;
     const uint16_t* cp = a.colpre + (f * a.nseg) * plane_sz + (int64_t)g * kGroup * a.Wp;
+    if constexpr (COLT) if (t > 0) {
+      // the carry also counts the pixels above the segment and left of the
+      // tile: the count kernel's per-chunk totals, segments s' < s, chunks
+      // left of the tile (spread over the CTA, reduced through sls[])
+      const int nch = (int)(a.Wp / kChunk), left = (int)(ct / kChunk);
+      uint4 part = make_uint4(0u, 0u, 0u, 0u);
+      const uint32_t* tt = a.chunktot + (f * a.nseg) * nch * a.nbp + g * kGroup;
+      for (int e = threadIdx.x; e < s * left; e += blockDim.x) {
+        const int sp = e / left, x = e - sp * left;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(tt + ((int64_t)sp * nch + x) * a.nbp));
+        part.x += v.x;
+        part.y += v.y;
+        part.z += v.z;
+        part.w += v.w;
+      }
+      part.x = __reduce_add_sync(kFull, part.x);
+      part.y = __reduce_add_sync(kFull, part.y);
+      part.z = __reduce_add_sync(kFull, part.z);
+      part.w = __reduce_add_sync(kFull, part.w);
+      if (lane == 0) sls[warp] = part;
+    }
     // prefix table: one slot; raw counts: sum slots 0..s-1 here (L2-resident),
     // U slots' loads in flight at a time (register budget bounds U)
     constexpr int U = CPL >= 4 ? 1 : 4;
@@ -558,24 +590,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
             acc[k][3][i] += v[u][k][i].y >> 16;
           }
     }
-    if (COLT && t > 0 && warp == 0) {
-      // the carry also counts the pixels above the segment and left of the
-      // tile: sum over segments s' < s of k2_rowleft's per-segment sums
-      uint4 part = make_uint4(0u, 0u, 0u, 0u);
-      const uint32_t* sl = a.segleft + (f * a.nseg * (a.T - 1) + (t - 1)) * a.nbp + g * kGroup;
-      for (int sp = lane; sp < s; sp += 32) {
-        const uint4 x = __ldg(reinterpret_cast<const uint4*>(sl + (int64_t)sp * (a.T - 1) * a.nbp));
-        part.x += x.x;
-        part.y += x.y;
-        part.z += x.z;
-        part.w += x.w;
-      }
-      part.x = __reduce_add_sync(kFull, part.x);
-      part.y = __reduce_add_sync(kFull, part.y);
-      part.z = __reduce_add_sync(kFull, part.z);
-      part.w = __reduce_add_sync(kFull, part.w);
-      if (lane == 0) sls[0] = part;
-    }
+
   }
 
   // COLT: row counts left of the tile (k2_rowleft), prefetched one batch ahead
@@ -737,11 +752,11 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     uint32_t wp[4] = {__reduce_add_sync(kFull, tw.x), __reduce_add_sync(kFull, tw.y),
                       __reduce_add_sync(kFull, tw.z), __reduce_add_sync(kFull, tw.w)};
     if (COLT && t > 0) {
-      const uint4 x = sls[0];
-      wp[0] += x.x;
-      wp[1] += x.y;
-      wp[2] += x.z;
-      wp[3] += x.w;
+      const uint4 x = lane < (int)(blockDim.x >> 5) ? sls[lane] : make_uint4(0u, 0u, 0u, 0u);
+      wp[0] += __reduce_add_sync(kFull, x.x);
+      wp[1] += __reduce_add_sync(kFull, x.y);
+      wp[2] += __reduce_add_sync(kFull, x.z);
+      wp[3] += __reduce_add_sync(kFull, x.w);
     }
 #pragma unroll
     for (int k = 0; k < CPL; ++k)

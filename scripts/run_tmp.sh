@@ -1,7 +1,7 @@
-mkdir -p gpurun_out/san
-for tool in memcheck racecheck synccheck; do
-  timeout 900 compute-sanitizer --tool $tool python scripts/sanitize_cases.py > gpurun_out/san/$tool.txt 2>&1; echo $tool=$?
+mkdir -p gpurun_out
+for tc in 16 8 4; do
+  IH_TILE_CHUNKS=$tc timeout 600 python scripts/graph_time.py 512 hd1 hd8 hd64 4k128 4k128/8 8k256/8 > gpurun_out/graph_tc$tc.jsonl 2>&1
 done
-timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_r01e_8k256.csv python bench.py --workload 8k256 --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1; echo l8k=$?
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:"k2_scan|k2_rowleft|k2_colcounts_all" -c 3 -o gpurun_out/prof_8k256 -f python scripts/one.py 8k256 > /dev/null 2>&1; echo ncu8k=$?
-timeout 400 ncu --set full --clock-control none --import-source on -k regex:"k2_scan|k2_colcounts_all" -c 2 -o gpurun_out/prof_hd64 -f python scripts/one.py hd64 > /dev/null 2>&1; echo ncuhd=$?
+for n in 17 34 68; do IH_MIN_SEG_ROWS=8 IH_NSEG=$n timeout 300 python scripts/graph_time.py hd1 >> gpurun_out/graph_hd1_nseg.jsonl 2>&1; done
+IH_TILE_CHUNKS=4 IH_PYTEST_QUICK=1 timeout 600 python -m pytest tests/test_parity_gpu.py -q -x -k "column_tiles or segments_and or config_checksums" > gpurun_out/pytest_tc4.log 2>&1; echo pytest=$?
+echo done
