@@ -576,6 +576,37 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   if (!t || !out) return fail(IH_ERR_PARAM, "null pointer");
   if (nb > 65535) return fail(IH_ERR_PARAM, "too many bins");
   const int64_t R = height - h + 1, C = width - w + 1;
+  // IH_K4_MODE: 1 (default) four-corner gathers, 4 outputs per thread;
+  // 2 staged row differences while CW + w u32 fit in shared memory; 0 the
+  // two-output four-corner kernel
+  const int threads = C >= 1024 ? 256 : (int)((C + 127) / 128 * 32);
+  const size_t smem = (size_t)(4 * threads + w) * sizeof(uint32_t);
+  const int64_t k4mode = env_int("IH_K4_MODE", 1);  // 0 corners, 1 ILP corners, 2 staged
+  if (k4mode == 1) {
+    // rows are grid-strided over ~64 CTAs per SM in total, so each CTA walks
+    // several rows (one-row CTAs: 0.52 of HBM, 148*64 CTAs: 0.59, HD x32)
+    const int64_t cb = (C + 1023) / 1024;
+    int64_t ry = (int64_t)kNumSMs * 64 / (cb * nb);
+    ry = ry < 1 ? 1 : ry > R ? R : ry > 65535 ? 65535 : ry;
+    ry = env_int("IH_K4_ROWS_GRID", ry);
+    dim3 grid((unsigned)cb, (unsigned)ry, (unsigned)nb);
+    ih::k4_window_counts_ilp<4><<<grid, 256, 0, (cudaStream_t)stream>>>(
+        t, nb, height, width, h, w, reinterpret_cast<long long*>(out));
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts_ilp");
+    return IH_OK;
+  }
+  if (smem <= 160 * 1024 && k4mode == 2) {
+    auto k = ih::k4_window_counts_vs;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+      return cuda_fail("k4 smem attribute");
+    const int64_t cblocks = (C + 4 * threads - 1) / (4 * threads);
+    dim3 grid((unsigned)cblocks, (unsigned)(R < 65535 ? R : 65535), (unsigned)nb);
+    k<<<grid, threads, smem, (cudaStream_t)stream>>>(t, nb, height, width, h, w,
+                                                     reinterpret_cast<long long*>(out));
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts_vs");
+    return IH_OK;
+  }
   dim3 grid((unsigned)((C + 511) / 512), (unsigned)(R < 65535 ? R : 65535), (unsigned)nb);
   ih::k4_window_counts<<<grid, 256, 0, (cudaStream_t)stream>>>(
       t, nb, height, width, h, w, reinterpret_cast<long long*>(out));
@@ -630,6 +661,8 @@ ih_status ih_likelihood_map(const uint32_t* t, int32_t nb, int64_t height, int64
   ih::Template tpl;
   for (int b = 0; b < 256; ++b) tpl.t[b] = b < nb ? template_host[b] : 0.0;
   const int64_t R = height - h + 1, C = width - w + 1;
+  // one row per CTA: K5 is FP64-issue bound (a true division and a sqrt per
+  // placement and bin) and wants every warp slot filled
   dim3 grid((unsigned)((C + 255) / 256), (unsigned)(R < 65535 ? R : 65535));
   if (metric == IH_METRIC_INTERSECTION)
     ih::k5_likelihood_map<true><<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h,

@@ -80,6 +80,97 @@ __global__ void __launch_bounds__(256) k4_window_counts(const uint32_t* __restri
   }
 }
 
+// K4 (ILP): as k4_window_counts with U outputs per thread (columns j + u*256),
+// all 4U corner loads issued before the first store: the corner reads are L2
+// hits, so memory-level parallelism per thread decides the throughput.
+template <int U>
+__global__ void __launch_bounds__(256) k4_window_counts_ilp(const uint32_t* __restrict__ t, int nb,
+                                                             int64_t H, int64_t W, int h, int w,
+                                                             long long* __restrict__ out) {
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const int64_t b = blockIdx.z;
+  const uint32_t* p = t + b * H * W;
+  for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
+    const uint32_t* bot = p + (i + h - 1) * W;
+    const uint32_t* topr = p + (i - 1) * W;  // used only when i > 0
+    long long* orow = out + (b * R + i) * C;
+    uint32_t a[U][4];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = ((int64_t)blockIdx.x * U + u) * blockDim.x + threadIdx.x;
+      const bool ok = j < C;
+      a[u][0] = ok ? __ldg(bot + j + w - 1) : 0u;
+      a[u][1] = ok && j > 0 ? __ldg(bot + j - 1) : 0u;
+      a[u][2] = ok && i > 0 ? __ldg(topr + j + w - 1) : 0u;
+      a[u][3] = ok && i > 0 && j > 0 ? __ldg(topr + j - 1) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = ((int64_t)blockIdx.x * U + u) * blockDim.x + threadIdx.x;
+      if (j < C)
+        __stcs(orow + j, (long long)a[u][0] - (long long)a[u][1] - (long long)a[u][2] +
+                             (long long)a[u][3]);
+    }
+  }
+}
+
+// Row-difference staging for K4 (the "vs" variant).  For output
+// row i the window count at column j is
+//     V[j + w - 1] - V[j - 1],   V(c) = T(i + h - 1, c) - T(i - 1, c)
+// (V(-1) = 0, T(-1, .) = 0).  V(c) counts the pixels of rows (i-1, i+h-1] in
+// columns [0, c], so 0 <= V <= h*(c+1) <= H*W <= 2^32-1: exact in u32, and the
+// difference of two V values is the exact (non-negative) window count.  A CTA
+// stages V for its column block once per (row, bin) with two coalesced row
+// reads instead of four corner gathers per output, then every thread forms 4
+// consecutive outputs from shared memory.
+//   CTA = (column block of CW = 4*blockDim outputs, output rows i (grid-stride)).
+//   smem: V for columns j0-1 .. j0+CW+w-2, i.e. CW + w u32 (x2 buffers in K5).
+__device__ __forceinline__ void stage_v(uint32_t* V, const uint32_t* bot, const uint32_t* top,
+                                        int64_t j0, int span) {
+  for (int k = threadIdx.x; k < span; k += blockDim.x) {
+    const int64_t c = j0 - 1 + k;
+    uint32_t v = 0u;
+    if (c >= 0) v = __ldg(bot + c) - (top ? __ldg(top + c) : 0u);
+    V[k] = v;
+  }
+}
+
+// K4 (staged): grid (column blocks, rows, bins); int64 out, 16-byte streaming
+// stores when the output row length C is even (every row start 16-B aligned).
+__global__ void __launch_bounds__(256) k4_window_counts_vs(const uint32_t* __restrict__ t, int nb,
+                                                            int64_t H, int64_t W, int h, int w,
+                                                            long long* __restrict__ out) {
+  extern __shared__ uint32_t V[];
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const int CW = 4 * blockDim.x;
+  const int64_t j0 = (int64_t)blockIdx.x * CW;
+  const int ncols = (int)min((int64_t)CW, C - j0);
+  const int span = ncols + w;
+  const int64_t b = blockIdx.z;
+  const uint32_t* p = t + b * H * W;
+  const bool vec = (C & 1) == 0;
+  for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
+    stage_v(V, p + (i + h - 1) * W, i > 0 ? p + (i - 1) * W : nullptr, j0, span);
+    __syncthreads();
+    const int q = 4 * threadIdx.x;
+    if (q < ncols) {
+      long long o[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) o[e] = q + e < ncols ? (long long)(V[q + e + w] - V[q + e]) : 0;
+      long long* dst = out + (b * R + i) * C + j0 + q;
+      if (vec && q + 4 <= ncols) {
+        __stcs(reinterpret_cast<longlong2*>(dst), make_longlong2(o[0], o[1]));
+        __stcs(reinterpret_cast<longlong2*>(dst) + 1, make_longlong2(o[2], o[3]));
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (q + e < ncols) __stcs(dst + e, o[e]);
+      }
+    }
+    __syncthreads();  // V is rewritten for the next row
+  }
+}
+
 // K5: fused likelihood map (likelihood.py:55-77).  One thread per window
 // placement (i, j), j fastest: for every bin b, the window count from four
 // corner reads, q = count / (h*w) (a true division, as numpy does), the metric

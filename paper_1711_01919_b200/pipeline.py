@@ -5,8 +5,8 @@ output dominates the traffic (4*B bytes per input byte), so the pipeline
 overlaps the device->host copy of chunk k with the kernel of chunk k+1 on a
 separate stream, through a two-slot device ring:
 
-    stream C : H2D(all frames)  K(0)  K(1)  K(2) ...
-    stream D :                        D2H(0) D2H(1) ...
+    stream C : H2D(0) K(0) H2D(1) K(1) H2D(2) K(2) ...
+    stream D :                  D2H(0)        D2H(1) ...
 
 Host buffers should be pinned (``pinned_empty``) for full PCIe bandwidth.
 """
@@ -70,9 +70,13 @@ class FramePipeline:
         Returns host_out after the last copy completed."""
         H, W = self.H, self.W
         slot_free = [None, None]
-        with torch.cuda.stream(self.s_comp):
-            self.d_in.copy_(host_frames, non_blocking=True)
+        uploaded = 0  # frames [0, uploaded) are on the device
         for k, (f0, f1, b0, b1) in enumerate(self.pieces):
+            if f1 > uploaded:  # upload a piece's frames just before its kernel: the
+                # H2D overlaps the previous piece's D2H (PCIe is full duplex)
+                with torch.cuda.stream(self.s_comp):
+                    self.d_in[uploaded:f1].copy_(host_frames[uploaded:f1], non_blocking=True)
+                uploaded = f1
             slot = k % 2
             n = (f1 - f0) * (b1 - b0) * H * W
             buf = self.ring[slot][:n].view(f1 - f0, b1 - b0, H, W)

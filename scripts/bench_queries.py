@@ -53,7 +53,10 @@ for (h, w) in ((64, 64), (8, 8)):
         q = device.window_counts(t, h, w).to(torch.float64) / float(h * w)
         return torch.sqrt(tt * q).sum(0).clamp_(0, 1)
     ms_u = timeit(unfused, reps=3)
+    alg5 = 32 * 1080 * 1920 * 4 + R * C * 8  # one read of the tensor + the f64 map
     res.append({"kernel": "k5_likelihood_map", "tensor": "1920x1080x32", "window": f"{h}x{w}",
                 "ms": round(ms, 4), "unfused_ms": round(ms_u, 4), "speedup": round(ms_u / ms, 1),
+                "alg_GBs": round(alg5 / ms / 1e6, 1), "frac": round(alg5 / ms / 1e6 / PEAK, 3),
                 "placements_per_s": round(R * C / ms * 1e3)})
-for r_ in res: print(json.dumps(r_), flush=True)
+tag = {k: os.environ[k] for k in ("IH_K4_MODE",) if k in os.environ}
+for r_ in res: print(json.dumps({**r_, **tag}), flush=True)

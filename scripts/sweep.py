@@ -22,6 +22,12 @@ WL = {
   "4k128/2": (3840, 2160, 128, 1, (0, 64)),
   "4k128/4": (3840, 2160, 128, 1, (0, 32)),
   "8k256": (8192, 8192, 256, 1, None),
+  "hd2": (1920, 1080, 32, 2, None),
+  "hd4": (1920, 1080, 32, 4, None),
+  "4k128/16": (3840, 2160, 128, 1, (0, 8)),
+  "8k256/2": (8192, 8192, 256, 1, (0, 128)),
+  "8k256/4": (8192, 8192, 256, 1, (0, 64)),
+  "512x8": (512, 512, 32, 8, None),
 }
 def run(name, reps=5, kernel="auto"):
     W, H, B, F, br = WL[name]

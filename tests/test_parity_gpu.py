@@ -26,7 +26,7 @@ def crc_of(t) -> str:
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
     for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
-              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB"):
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -435,6 +435,21 @@ def test_out_argument_and_int32_view(rng):
     with pytest.raises(ih.ShapeError):
         device.integral_histogram(device.upload_image(px), lut, 5,
                                   out=torch.zeros((1, 4, 50, 70), dtype=torch.int32, device="cuda"))
+
+
+def test_window_count_kernel_variants(monkeypatch, rng):
+    """K4 variants (two-output corners, 4-output ILP corners, staged row
+    differences) against the oracle: bit-identical, including odd output
+    widths, w = W, h = H and 1-pixel windows."""
+    for (H, W, B) in [(70, 1500, 5), (33, 2100, 32), (9, 7, 3), (300, 257, 16)]:
+        px = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        full = O.compute_crossweave(px, O.np_uniform_table(B), B)
+        t = torch.from_numpy(full.view(np.int32)).cuda().view(torch.uint32)
+        for (h, w) in [(1, 1), (min(5, H), min(8, W)), (H, W), (H // 2 + 1, W // 3 + 1), (1, W), (H, 1)]:
+            want = O.window_counts(full, h, w)
+            for mode in ("0", "1", "2"):
+                monkeypatch.setenv("IH_K4_MODE", mode)
+                assert np.array_equal(device.window_counts(t, h, w).cpu().numpy(), want), (H, W, h, w, mode)
 
 
 @pytest.mark.parametrize("metric", ["intersection", "bhattacharyya"])
