@@ -283,6 +283,10 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     out = device.empty_output(max(nloc, 1), max(nb, 1), wl.height, wl.width, dev)
     stream = torch.cuda.current_stream(dev)
     brange = (b0, b1) if active else None
+    tuned = None
+    if args.autotune and active:  # measured row-segment count for this shape (warm-up phase)
+        tuned = device.autotune(nloc, wl.height, wl.width, wl.bins, bin_range=brange, device=dev,
+                                images=d_img[:nloc], out=out[:nloc])
     plan = device.plan(nloc, wl.height, wl.width, nb,
                        aligned16=d_img.data_ptr() % 16 == 0) if active else {"launches": 0}
 
@@ -395,6 +399,7 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
         "pipelined_steps": bool(args.overlap),
         "gpu_launches": plan["launches"] * args.steps,
         "plan": plan,
+        "autotune": tuned,
         "parity": "rank-0 output crc32 == reference golden" if not bad else "MISMATCH",
         "clocks": clocks.summary(),
     }
@@ -462,6 +467,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=4, help="frames per pipelined e2e chunk")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--no-autotune", dest="autotune", action="store_false",
+                    help="keep the planner's heuristic row-segment count")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false",
                     help="run each step's prepass and scan back to back on one stream")
     ap.add_argument("--ref-budget", type=float, default=10.0,

@@ -105,9 +105,18 @@ ih_status ih_ih_scan(const uint8_t *img, int64_t frames, int64_t height, int64_t
  *   info[4] 128-column chunks per lane       info[5] rows per barrier batch
  *   info[6] warps per CTA                    info[7] workspace bytes needed
  *   info[8] column tiles per row             info[9] tile width (columns)
- * (`info` holds 10 entries.)  Same shape/parameter errors as ih_integral_histogram. */
+ *   info[10] resident scan CTAs (SMs x CTAs/SM)  info[11] scan CTAs per row segment
+ * (`info` holds 12 entries.)  Same shape/parameter errors as ih_integral_histogram. */
 ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
                            int32_t kernel, int32_t aligned16, int64_t *info);
+
+/* Row-segment hint for one problem shape (frames, height, width, slab bins):
+ * ih_integral_histogram then splits each frame into `nseg` row segments
+ * instead of its heuristic choice (results are identical for every count;
+ * only speed changes).  nseg = 0 removes the hint.  A small process-wide
+ * table guarded by a mutex; device.autotune() fills it from measurements. */
+ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
+                       int32_t nseg);
 
 /* Batched four-corner region queries (core.py:179-195).
  *   t        device (nb, height, width) uint32 integral histogram (a slab is fine)

@@ -36,6 +36,7 @@ EXPORTS = (
     "ih_region_histograms",
     "ih_window_counts",
     "ih_plan_describe",
+    "ih_plan_hint",
     "ih_likelihood_map",
     "ih_status_string",
     "ih_last_error",
@@ -77,6 +78,8 @@ def lib() -> ctypes.CDLL:
     L.ih_likelihood_map.restype = ctypes.c_int
     L.ih_plan_describe.argtypes = [i64, i64, i64, i32, i32, i32, P]
     L.ih_plan_describe.restype = ctypes.c_int
+    L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32]
+    L.ih_plan_hint.restype = ctypes.c_int
     L.ih_status_string.argtypes = [ctypes.c_int]
     L.ih_status_string.restype = ctypes.c_char_p
     L.ih_last_error.argtypes = []

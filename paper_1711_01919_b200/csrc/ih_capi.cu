@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <utility>
 
 #include "../../include/inthist_b200.h"
@@ -35,6 +36,25 @@ int64_t env_int(const char* name, int64_t dflt) {
 }
 
 constexpr int kNumSMs = 148;
+
+// Row-segment hints (ih_plan_hint): measured segment counts per problem shape,
+// set by an autotuner; consulted by plan_k2 before its own heuristic.
+struct PlanHint {
+  int64_t frames, H, W;
+  int32_t nb, nseg;
+};
+constexpr int kMaxHints = 64;
+PlanHint g_hints[kMaxHints];
+int g_nhints = 0;
+std::mutex g_hint_mu;
+
+int32_t hint_lookup(int64_t frames, int64_t H, int64_t W, int32_t nb) {
+  std::lock_guard<std::mutex> lock(g_hint_mu);
+  for (int i = 0; i < g_nhints; ++i)
+    if (g_hints[i].frames == frames && g_hints[i].H == H && g_hints[i].W == W && g_hints[i].nb == nb)
+      return g_hints[i].nseg;
+  return 0;
+}
 
 // Launch with programmatic stream serialization when `pdl` (see ih_kernels.cuh
 // griddep_wait): only for a kernel whose stream predecessor is a kernel this
@@ -68,6 +88,8 @@ struct K2Plan {
   int T = 1;         // column tiles (colt)
   int TW = 0;        // tile width = nwarps * cpl * 128
   bool colt = false; // column-tiled instantiation (W > 2048 unless IH_NO_COLTILE)
+  int slots = 0;     // resident CTAs of the scan kernel (SMs x CTAs per SM)
+  int64_t units = 0; // scan CTAs per row segment (frames x bin groups x tiles)
   int carry = 0;     // ih::Carry: NONE (nseg == 1), TABLE or LOOKBACK
   bool big = false;  // 1024-thread instantiation (up to 32 warps, <= 64 registers)
   bool vec = true;   // W % 4 == 0
@@ -220,6 +242,10 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (nseg > max_seg) nseg = max_seg;
   if (nseg > 65535) nseg = 65535;
   if (nseg < 1) nseg = 1;
+  p.slots = (int)slots;
+  p.units = units;
+  const int32_t hinted = hint_lookup(frames, H, W, nb);
+  if (hinted > 0) nseg = hinted < H ? hinted : H;
   const int64_t forced = env_int("IH_NSEG", 0);
   if (forced > 0) nseg = forced < H ? forced : H;
   // u16 count tables: a segment has < 65536 rows; images taller than 65535
@@ -626,7 +652,7 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   const bool tma = aligned16 != 0 && env_int("IH_NO_TMA", 0) == 0;
   K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0, tma);
   const int k = resolve_kernel(kernel, p);
-  for (int i = 0; i < 10; ++i) info[i] = 0;
+  for (int i = 0; i < 12; ++i) info[i] = 0;
   info[0] = k;
   if (k == IH_KERNEL_CROSSWEAVE) {
     info[1] = height > 1 ? 2 : 1;
@@ -645,6 +671,8 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   info[7] = (int64_t)k2_ws_bytes(frames, height, p);
   info[8] = p.T;
   info[9] = p.TW;
+  info[10] = p.slots;
+  info[11] = p.units;
   return IH_OK;
 }
 
@@ -674,6 +702,29 @@ ih_status ih_likelihood_map(const uint32_t* t, int32_t nb, int64_t height, int64
   return IH_OK;
 }
 
+ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
+                       int32_t nseg) {
+  if (frames < 1 || height < 1 || width < 1) return fail(IH_ERR_SHAPE, "image must be non-empty");
+  if (slab_bins < 1 || slab_bins > 256) return fail(IH_ERR_SHAPE, "bin count must be in [1, 256]");
+  if (nseg < 0) return fail(IH_ERR_PARAM, "negative segment count");
+  std::lock_guard<std::mutex> lock(g_hint_mu);
+  for (int i = 0; i < g_nhints; ++i) {
+    PlanHint& h = g_hints[i];
+    if (h.frames == frames && h.H == height && h.W == width && h.nb == slab_bins) {
+      if (nseg > 0) {
+        h.nseg = nseg;
+      } else {
+        h = g_hints[--g_nhints];
+      }
+      return IH_OK;
+    }
+  }
+  if (nseg == 0) return IH_OK;
+  if (g_nhints == kMaxHints) g_nhints = 0;  // a small cache: start over when full
+  g_hints[g_nhints++] = PlanHint{frames, height, width, slab_bins, nseg};
+  return IH_OK;
+}
+
 const char* ih_status_string(ih_status s) {
   switch (s) {
     case IH_OK: return "IH_OK";
@@ -688,6 +739,6 @@ const char* ih_status_string(ih_status s) {
 
 const char* ih_last_error(void) { return g_last_error; }
 
-int32_t ih_abi_version(void) { return (1 << 16) | 1; }
+int32_t ih_abi_version(void) { return (1 << 16) | 2; }
 
 }  // extern "C"

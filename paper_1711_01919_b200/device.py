@@ -101,7 +101,8 @@ def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel
 
 
 PLAN_FIELDS = ("kernel", "launches", "segments", "segment_rows", "chunks_per_lane",
-               "rows_per_batch", "warps_per_cta", "workspace_bytes", "column_tiles", "tile_width")
+               "rows_per_batch", "warps_per_cta", "workspace_bytes", "column_tiles", "tile_width",
+               "resident_ctas", "ctas_per_segment")
 
 
 def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto",
@@ -113,6 +114,83 @@ def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "au
     d = dict(zip(PLAN_FIELDS, list(info)))
     d["kernel"] = {v: k for k, v in _native.KERNELS.items()}[d["kernel"]]
     return d
+
+
+def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments: int) -> None:
+    """Pin the row-segment count for one problem shape (0 removes the pin)."""
+    _native.check(_native.lib().ih_plan_hint(frames, height, width, slab_bins, int(segments)))
+
+
+def segment_candidates(frames: int, height: int, width: int, slab_bins: int) -> list:
+    """Row-segment counts worth measuring for a shape: the heuristic's choice and
+    the counts whose scan grid ends just at (or just below) a whole number of
+    waves of resident CTAs, 1..12 waves, segments of >= 32 rows."""
+    p = plan(frames, height, width, slab_bins)
+    if p["kernel"] != "single_pass":
+        return []
+    slots, units = max(1, p["resident_ctas"]), max(1, p["ctas_per_segment"])
+    max_seg = max(1, -(-height // 32))
+    cands = {p["segments"]}
+    for waves in range(1, 13):
+        n = (waves * slots) // units
+        for m in (n, n - 1):
+            if 1 <= m <= max_seg:
+                cands.add(m)
+    return sorted(cands)
+
+
+def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, device=None,
+             candidates=None, reps: int = 5, images=None, out=None) -> dict:
+    """Measure integral_histogram (prepare + scan, CUDA-graph replay) for each
+    candidate row-segment count on random frames of this shape, pin the fastest
+    with set_plan_hint, and return {"segments": best, "ms": {count: ms}}.
+    Results are bit-identical for every count; only the speed differs.
+    ``images`` / ``out`` (CUDA tensors of the call's shapes) avoid allocating
+    a second input and output."""
+    dev = require_cuda(device)
+    lo, hi = (0, bins) if bin_range is None else bin_range
+    nb = hi - lo
+    if candidates is None:
+        candidates = segment_candidates(frames, height, width, nb)
+    if not candidates:
+        return {"segments": None, "ms": {}}
+    if images is None:
+        gen = torch.Generator(device=dev).manual_seed(1234)
+        images = torch.randint(0, 256, (frames, height, width), dtype=torch.uint8, device=dev,
+                               generator=gen)
+    imgs = images
+    lut = ((np.arange(256) * bins) // 256).astype(np.uint8)
+    if out is None:
+        out = empty_output(frames, nb, height, width, dev)
+    need = 16
+    for n in candidates:  # the workspace grows with the segment count
+        set_plan_hint(frames, height, width, nb, n)
+        need = max(need, workspace_bytes(frames, height, width, nb))
+    ws = torch.empty(need, dtype=torch.uint8, device=dev)
+    side = torch.cuda.Stream(dev)
+    times = {}
+    with torch.cuda.device(dev):
+        for n in candidates:
+            set_plan_hint(frames, height, width, nb, n)
+            for _ in range(2):  # warm: attributes, caches
+                integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=ws)
+            torch.cuda.synchronize(dev)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=ws)
+            g.replay()
+            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+            torch.cuda.synchronize(dev)
+            e0.record()
+            for _ in range(reps):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize(dev)
+            times[n] = e0.elapsed_time(e1) / reps
+            del g
+    best = min(times, key=times.get)
+    set_plan_hint(frames, height, width, nb, best)
+    return {"segments": best, "ms": {int(k): round(v, 4) for k, v in times.items()}}
 
 
 def empty_output(frames: int, slab_bins: int, height: int, width: int, device) -> torch.Tensor:

@@ -1,5 +1,7 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -k "variants or window or likelihood or small_case_queries" > gpurun_out/pytest_q.log 2>&1; echo pytest=$?
-(timeout 600 python scripts/bench_queries.py 2>&1 | grep "k4_\|k5_"
-for ry in 8 32 128 1017; do IH_K4_ROWS_GRID=$ry IH_K5_ROWS_GRID=$ry timeout 600 python scripts/bench_queries.py 2>&1 | grep "k4_\|k5_" | sed "s/^/ry$ry /"; done) > gpurun_out/queries_k4ry.jsonl
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -k "autotune or plan_describe or graph" > gpurun_out/pytest_at.log 2>&1; echo pytest=$?
+timeout 900 python bench.py --e2e-steps 1 > gpurun_out/bench_at_hd64.json 2> gpurun_out/bench_at_hd64.err; echo b1=$?
+for fr in 32 16 8; do timeout 900 python bench.py --frames $fr --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_at_hd$fr.json 2>> gpurun_out/bench_at.err; done
+timeout 900 python bench.py --workload 4k128 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_at_4k128.json 2>> gpurun_out/bench_at.err
+timeout 900 python bench.py --workload 8k256 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_at_8k256.json 2>> gpurun_out/bench_at.err
 echo done

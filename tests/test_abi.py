@@ -123,3 +123,20 @@ def test_column_tile_plan():
     assert (p["column_tiles"], p["tile_width"]) == (1, 1920)
     p = device.plan(1, 3, 30001, 4)
     assert p["column_tiles"] * p["tile_width"] >= 30001 and p["tile_width"] <= 2048
+
+
+def test_plan_hint_overrides_segments():
+    """ih_plan_hint pins the row-segment count for one shape only; 0 removes it."""
+    from paper_1711_01919_b200 import device
+
+    base = device.plan(8, 1080, 1920, 32)["segments"]
+    device.set_plan_hint(8, 1080, 1920, 32, 5)
+    try:
+        assert device.plan(8, 1080, 1920, 32)["segments"] == 5
+        assert device.plan(8, 1080, 1920, 16)["segments"] == device.plan(8, 1080, 1920, 16)["segments"]
+        assert device.plan(9, 1080, 1920, 32)["segments"] != 5 or base == 5
+    finally:
+        device.set_plan_hint(8, 1080, 1920, 32, 0)
+    assert device.plan(8, 1080, 1920, 32)["segments"] == base
+    cands = device.segment_candidates(8, 1080, 1920, 32)
+    assert base in cands and all(1 <= n <= 34 for n in cands)

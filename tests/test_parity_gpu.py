@@ -417,6 +417,21 @@ def test_cuda_graph_capture_and_streams(frames, h, w, bins, rng):
             assert np.array_equal(out[f].cpu().numpy(), O.compute_crossweave(new[f], lut, bins))
 
 
+def test_autotune_pins_a_measured_segment_count(rng):
+    """device.autotune times candidate row-segment counts and pins the fastest;
+    the pinned plan still produces the oracle's tensor."""
+    res = device.autotune(3, 300, 700, 12)
+    try:
+        assert res["segments"] in res["ms"] and len(res["ms"]) >= 1
+        assert device.plan(3, 300, 700, 12)["segments"] == res["segments"]
+        frames = rng.integers(0, 256, (3, 300, 700), dtype=np.uint8)
+        t = ih.compute_frames(frames, ih.BinSpec.uniform(12))
+        for f in range(3):
+            assert np.array_equal(t[f].cpu().numpy(), O.compute_crossweave(frames[f], O.np_uniform_table(12), 12))
+    finally:
+        device.set_plan_hint(3, 300, 700, 12, 0)
+
+
 def test_plan_describe_matches_launches():
     p = device.plan(64, 1080, 1920, 32)
     assert p["kernel"] == "single_pass" and p["launches"] in (1, 2, 3)
