@@ -19,7 +19,8 @@
  * Conventions (all entry points):
  *   - stream-ordered and asynchronous: work is enqueued on `stream`; nothing
  *     synchronises the host; no allocation (the caller owns every buffer,
- *     including the workspace); no global state.
+ *     including the workspace); no global state except the optional
+ *     row-segment hint table of ih_plan_hint.
  *   - all pointers except `lut256` are DEVICE pointers; sizes in elements
  *     unless suffixed _bytes.
  *   - argument validation mirrors the reference's exception order; every
@@ -148,6 +149,17 @@ typedef enum { IH_METRIC_INTERSECTION = 0, IH_METRIC_BHATTACHARYYA = 1 } ih_metr
 ih_status ih_likelihood_map(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
                             int32_t h, int32_t w, const double *template_host, int32_t metric,
                             double *out, void *stream);
+
+/* The same map through a per-(bin, count) metric table held in `workspace`
+ * (device, >= ih_likelihood_workspace_bytes(nb, h, w) bytes, 8-byte aligned):
+ * every window count lies in [0, h*w], so each term is computed once and the
+ * map kernel only gathers -- bit-identical to ih_likelihood_map.  With a
+ * smaller (or null) workspace it computes the terms directly. */
+size_t ih_likelihood_workspace_bytes(int32_t nb, int32_t h, int32_t w);
+ih_status ih_likelihood_map_ws(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
+                               int32_t h, int32_t w, const double *template_host, int32_t metric,
+                               double *out, void *workspace, size_t workspace_bytes,
+                               void *stream);
 
 /* Human-readable status name. */
 const char *ih_status_string(ih_status s);

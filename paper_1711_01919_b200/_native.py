@@ -38,6 +38,8 @@ EXPORTS = (
     "ih_plan_describe",
     "ih_plan_hint",
     "ih_likelihood_map",
+    "ih_likelihood_map_ws",
+    "ih_likelihood_workspace_bytes",
     "ih_status_string",
     "ih_last_error",
     "ih_abi_version",
@@ -76,6 +78,10 @@ def lib() -> ctypes.CDLL:
     L.ih_window_counts.restype = ctypes.c_int
     L.ih_likelihood_map.argtypes = [P, i32, i64, i64, i32, i32, P, i32, P, P]
     L.ih_likelihood_map.restype = ctypes.c_int
+    L.ih_likelihood_map_ws.argtypes = [P, i32, i64, i64, i32, i32, P, i32, P, P, ctypes.c_size_t, P]
+    L.ih_likelihood_map_ws.restype = ctypes.c_int
+    L.ih_likelihood_workspace_bytes.argtypes = [i32, i32, i32]
+    L.ih_likelihood_workspace_bytes.restype = ctypes.c_size_t
     L.ih_plan_describe.argtypes = [i64, i64, i64, i32, i32, i32, P]
     L.ih_plan_describe.restype = ctypes.c_int
     L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32]

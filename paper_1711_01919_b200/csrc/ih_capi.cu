@@ -676,9 +676,23 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   return IH_OK;
 }
 
+size_t ih_likelihood_workspace_bytes(int32_t nb, int32_t h, int32_t w) {
+  if (nb < 1 || nb > 256 || h < 1 || w < 1) return 0;
+  const uint64_t bytes = (uint64_t)nb * ((uint64_t)h * (uint64_t)w + 1) * sizeof(double);
+  return bytes <= (512ull << 20) ? (size_t)bytes : 0;  // no table for huge windows
+}
+
 ih_status ih_likelihood_map(const uint32_t* t, int32_t nb, int64_t height, int64_t width,
                             int32_t h, int32_t w, const double* template_host, int32_t metric,
                             double* out, void* stream) {
+  return ih_likelihood_map_ws(t, nb, height, width, h, w, template_host, metric, out, nullptr, 0,
+                              stream);
+}
+
+ih_status ih_likelihood_map_ws(const uint32_t* t, int32_t nb, int64_t height, int64_t width,
+                               int32_t h, int32_t w, const double* template_host, int32_t metric,
+                               double* out, void* workspace, size_t workspace_bytes,
+                               void* stream) {
   if (nb < 1 || nb > 256) return fail(IH_ERR_SHAPE, "bin count must be in [1, 256]");
   if (!template_host) return fail(IH_ERR_SHAPE, "null template");
   if (metric != IH_METRIC_INTERSECTION && metric != IH_METRIC_BHATTACHARYYA)
@@ -689,6 +703,25 @@ ih_status ih_likelihood_map(const uint32_t* t, int32_t nb, int64_t height, int64
   ih::Template tpl;
   for (int b = 0; b < 256; ++b) tpl.t[b] = b < nb ? template_host[b] : 0.0;
   const int64_t R = height - h + 1, C = width - w + 1;
+  const size_t tab = ih_likelihood_workspace_bytes(nb, h, w);
+  if (tab && workspace && workspace_bytes >= tab && env_int("IH_K5_DIRECT", 0) == 0) {
+    double* M = (double*)workspace;
+    const int64_t total = (int64_t)nb * ((int64_t)h * w + 1);
+    int64_t blocks = (total + 255) / 256;
+    if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+    if (metric == IH_METRIC_INTERSECTION)
+      ih::k5_metric_table<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+          tpl, nb, (int64_t)h * w, M);
+    else
+      ih::k5_metric_table<false><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
+          tpl, nb, (int64_t)h * w, M);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k5_metric_table");
+    dim3 grid((unsigned)((C + 255) / 256), (unsigned)(R < 65535 ? R : 65535));
+    ih::k5_likelihood_map_tab<<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h, w,
+                                                                      M, out);
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k5_likelihood_map_tab");
+    return IH_OK;
+  }
   // one row per CTA: K5 is FP64-issue bound (a true division and a sqrt per
   // placement and bin) and wants every warp slot filled
   dim3 grid((unsigned)((C + 255) / 256), (unsigned)(R < 65535 ? R : 65535));

@@ -223,4 +223,69 @@ __global__ void __launch_bounds__(256) k5_likelihood_map(const uint32_t* __restr
   }
 }
 
+// K5 with a metric table.  Every window count n lies in [0, h*w], so the
+// per-(bin, n) term M[b][n] = min(t_b, n/(h*w)) or sqrt(t_b * (n/(h*w))) is
+// computed once (k5_metric_table, the exact expressions of k5_likelihood_map)
+// and the map kernel only gathers: 4 corner reads, one table read (the bin's
+// slice is L1/L2-resident while the CTA's threads walk that bin) and an add,
+// in bin order -- bit-identical to k5_likelihood_map, without its per-element
+// FP64 division and square root.
+template <bool INTERSECTION>
+__global__ void __launch_bounds__(256) k5_metric_table(Template tpl, int nb, int64_t area,
+                                                        double* __restrict__ M) {
+  const int64_t n1 = area + 1;
+  const int64_t total = (int64_t)nb * n1;
+  const double a = (double)area;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(e / n1);
+    const int64_t n = e - b * n1;
+    const double q = (double)(long long)n / a;
+    const double tb = tpl.t[b];
+    M[e] = INTERSECTION ? fmin(tb, q) : sqrt(tb * q);
+  }
+}
+
+__global__ void __launch_bounds__(256) k5_likelihood_map_tab(const uint32_t* __restrict__ t, int nb,
+                                                              int64_t H, int64_t W, int h, int w,
+                                                              const double* __restrict__ M,
+                                                              double* __restrict__ out) {
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const int64_t n1 = (int64_t)h * w + 1;
+  const int64_t plane = H * W;
+  for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= C) continue;
+    const int64_t o11 = (i + h - 1) * W + (j + w - 1);
+    const int64_t o01 = (i - 1) * W + (j + w - 1);
+    const int64_t o10 = (i + h - 1) * W + (j - 1);
+    const int64_t o00 = (i - 1) * W + (j - 1);
+    double acc = 0.0;
+    constexpr int U = 8;  // bins per step: 32 corner loads, then 8 table loads in flight
+    for (int b0 = 0; b0 < nb; b0 += U) {
+      uint32_t n[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u < nb ? b0 + u : nb - 1;
+        const uint32_t* p = t + (int64_t)b * plane;
+        const uint32_t a11 = __ldg(p + o11);
+        const uint32_t a10 = j > 0 ? __ldg(p + o10) : 0u;
+        const uint32_t a01 = i > 0 ? __ldg(p + o01) : 0u;
+        const uint32_t a00 = i > 0 && j > 0 ? __ldg(p + o00) : 0u;
+        n[u] = a11 - a10 - a01 + a00;  // exact window count in [0, h*w]
+      }
+      double m[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u < nb ? b0 + u : nb - 1;
+        m[u] = __ldg(M + (int64_t)b * n1 + n[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)  // the sum over bins stays in order b = 0..nb-1
+        if (b0 + u < nb) acc += m[u];
+    }
+    out[i * C + j] = fmin(fmax(acc, 0.0), 1.0);
+  }
+}
+
 }  // namespace ih

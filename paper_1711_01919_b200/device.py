@@ -338,10 +338,15 @@ def likelihood_map(t: torch.Tensor, template, h: int, w: int, metric: str = "bha
     if h > H or w > W:
         raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
     out = torch.empty((H - h + 1, W - w + 1), dtype=torch.float64, device=t.device)
+    L = _native.lib()
+    nws = int(L.ih_likelihood_workspace_bytes(nb, int(h), int(w)))
     with torch.cuda.device(t.device):
-        _native.check(_native.lib().ih_likelihood_map(
+        ws = torch.empty(max(nws, 16), dtype=torch.uint8, device=t.device)  # stream-ordered reuse
+        _native.check(L.ih_likelihood_map_ws(
             t.data_ptr(), nb, H, W, int(h), int(w), tmpl.ctypes.data, metrics[metric],
-            out.data_ptr(), _stream_handle(t.device, stream)))
+            out.data_ptr(), ws.data_ptr(), nws, _stream_handle(t.device, stream)))
+        if stream is not None:
+            ws.record_stream(stream)  # freed at return: keep it until `stream` is done
     return out
 
 

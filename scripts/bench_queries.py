@@ -58,5 +58,5 @@ for (h, w) in ((64, 64), (8, 8)):
                 "ms": round(ms, 4), "unfused_ms": round(ms_u, 4), "speedup": round(ms_u / ms, 1),
                 "alg_GBs": round(alg5 / ms / 1e6, 1), "frac": round(alg5 / ms / 1e6 / PEAK, 3),
                 "placements_per_s": round(R * C / ms * 1e3)})
-tag = {k: os.environ[k] for k in ("IH_K4_MODE",) if k in os.environ}
+tag = {k: os.environ[k] for k in ("IH_K4_MODE", "IH_K5_DIRECT") if k in os.environ}
 for r_ in res: print(json.dumps({**r_, **tag}), flush=True)

@@ -1,6 +1,4 @@
 mkdir -p gpurun_out
-for fr in 8 16 32 64; do
-  timeout 900 python bench.py --frames $fr --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_ts0_hd$fr.json 2>> gpurun_out/bench_ts.err
-  IH_TABLE_SUM_MAX=1 timeout 900 python bench.py --frames $fr --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_ts1_hd$fr.json 2>> gpurun_out/bench_ts.err
-done
+timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -k "likelihood or variants or window" > gpurun_out/pytest_k5.log 2>&1; echo pytest=$?
+(timeout 600 python scripts/bench_queries.py 2>&1 | grep "k5_"; IH_K5_DIRECT=1 timeout 600 python scripts/bench_queries.py 2>&1 | grep "k5_") > gpurun_out/queries_k5tab.jsonl
 echo done

@@ -26,7 +26,7 @@ def crc_of(t) -> str:
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
     for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
-              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE"):
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -465,6 +465,23 @@ def test_window_count_kernel_variants(monkeypatch, rng):
             for mode in ("0", "1", "2"):
                 monkeypatch.setenv("IH_K4_MODE", mode)
                 assert np.array_equal(device.window_counts(t, h, w).cpu().numpy(), want), (H, W, h, w, mode)
+
+
+def test_likelihood_table_path_bit_identical(monkeypatch, rng):
+    """K5 through the per-(bin, count) metric table == K5 computing each term
+    directly (IH_K5_DIRECT=1), bit for bit, both metrics, several windows."""
+    for (H, W, B) in [(60, 90, 16), (40, 300, 256), (7, 9, 3)]:
+        px = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        t = torch.from_numpy(O.compute_crossweave(px, O.np_uniform_table(B), B).view(np.int32)).cuda().view(torch.uint32)
+        tmpl = rng.random(B)
+        tmpl /= tmpl.sum()
+        for (h, w) in [(1, 1), (min(8, H), min(8, W)), (H, W), (3, 7)]:
+            for m in ("intersection", "bhattacharyya"):
+                monkeypatch.delenv("IH_K5_DIRECT", raising=False)
+                a = device.likelihood_map(t, tmpl, h, w, m).cpu().numpy()
+                monkeypatch.setenv("IH_K5_DIRECT", "1")
+                b = device.likelihood_map(t, tmpl, h, w, m).cpu().numpy()
+                assert np.array_equal(a.view(np.int64), b.view(np.int64)), (H, W, B, h, w, m)
 
 
 @pytest.mark.parametrize("metric", ["intersection", "bhattacharyya"])
