@@ -107,17 +107,20 @@ ih_status ih_ih_scan(const uint8_t *img, int64_t frames, int64_t height, int64_t
  *   info[6] warps per CTA                    info[7] workspace bytes needed
  *   info[8] column tiles per row             info[9] tile width (columns)
  *   info[10] resident scan CTAs (SMs x CTAs/SM)  info[11] scan CTAs per row segment
- * (`info` holds 12 entries.)  Same shape/parameter errors as ih_integral_histogram. */
+ *   info[12] big segments (the rest are tail segments)  info[13] tail segment rows
+ * (`info` holds 14 entries.)  Same shape/parameter errors as ih_integral_histogram. */
 ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
                            int32_t kernel, int32_t aligned16, int64_t *info);
 
 /* Row-segment hint for one problem shape (frames, height, width, slab bins):
  * ih_integral_histogram then splits each frame into `nseg` row segments
- * instead of its heuristic choice (results are identical for every count;
- * only speed changes).  nseg = 0 removes the hint.  A small process-wide
- * table guarded by a mutex; device.autotune() fills it from measurements. */
+ * instead of its heuristic choice; with tail_pct > 0 the last ~tail_pct % of
+ * the rows become short segments of 1/tail_div the height (0: 4), which the
+ * segment-major scan grid runs last.  Results are identical for every choice;
+ * only speed changes.  nseg = 0 removes the hint.  A small process-wide table
+ * guarded by a mutex; device.autotune() fills it from measurements. */
 ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
-                       int32_t nseg);
+                       int32_t nseg, int32_t tail_pct, int32_t tail_div);
 
 /* Batched four-corner region queries (core.py:179-195).
  *   t        device (nb, height, width) uint32 integral histogram (a slab is fine)
@@ -160,6 +163,11 @@ ih_status ih_likelihood_map_ws(const uint32_t *t, int32_t nb, int64_t height, in
                                int32_t h, int32_t w, const double *template_host, int32_t metric,
                                double *out, void *workspace, size_t workspace_bytes,
                                void *stream);
+
+/* Debug: when set, k2_scan writes {start ns, prologue-done ns, end ns, SM id}
+ * (4 u64) per CTA into the device buffer (grids of at most `ctas` CTAs).
+ * NULL turns it off.  Not for production use (adds a barrier per CTA). */
+void ih_debug_trace(void *device_buffer, size_t ctas);
 
 /* Human-readable status name. */
 const char *ih_status_string(ih_status s);

@@ -38,6 +38,7 @@ EXPORTS = (
     "ih_plan_describe",
     "ih_plan_hint",
     "ih_likelihood_map",
+    "ih_debug_trace",
     "ih_likelihood_map_ws",
     "ih_likelihood_workspace_bytes",
     "ih_status_string",
@@ -78,13 +79,15 @@ def lib() -> ctypes.CDLL:
     L.ih_window_counts.restype = ctypes.c_int
     L.ih_likelihood_map.argtypes = [P, i32, i64, i64, i32, i32, P, i32, P, P]
     L.ih_likelihood_map.restype = ctypes.c_int
+    L.ih_debug_trace.argtypes = [P, ctypes.c_size_t]
+    L.ih_debug_trace.restype = None
     L.ih_likelihood_map_ws.argtypes = [P, i32, i64, i64, i32, i32, P, i32, P, P, ctypes.c_size_t, P]
     L.ih_likelihood_map_ws.restype = ctypes.c_int
     L.ih_likelihood_workspace_bytes.argtypes = [i32, i32, i32]
     L.ih_likelihood_workspace_bytes.restype = ctypes.c_size_t
     L.ih_plan_describe.argtypes = [i64, i64, i64, i32, i32, i32, P]
     L.ih_plan_describe.restype = ctypes.c_int
-    L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32]
+    L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32, i32, i32]
     L.ih_plan_hint.restype = ctypes.c_int
     L.ih_status_string.argtypes = [ctypes.c_int]
     L.ih_status_string.restype = ctypes.c_char_p

@@ -41,18 +41,25 @@ constexpr int kNumSMs = 148;
 // set by an autotuner; consulted by plan_k2 before its own heuristic.
 struct PlanHint {
   int64_t frames, H, W;
-  int32_t nb, nseg;
+  int32_t nb, nseg, tail_pct, tail_div;
 };
 constexpr int kMaxHints = 64;
 PlanHint g_hints[kMaxHints];
 int g_nhints = 0;
 std::mutex g_hint_mu;
 
-int32_t hint_lookup(int64_t frames, int64_t H, int64_t W, int32_t nb) {
+unsigned long long* g_trace = nullptr;  // ih_debug_trace
+size_t g_trace_ctas = 0;
+
+int32_t hint_lookup(int64_t frames, int64_t H, int64_t W, int32_t nb, int32_t* tail_pct,
+                    int32_t* tail_div) {
   std::lock_guard<std::mutex> lock(g_hint_mu);
   for (int i = 0; i < g_nhints; ++i)
-    if (g_hints[i].frames == frames && g_hints[i].H == H && g_hints[i].W == W && g_hints[i].nb == nb)
+    if (g_hints[i].frames == frames && g_hints[i].H == H && g_hints[i].W == W && g_hints[i].nb == nb) {
+      *tail_pct = g_hints[i].tail_pct;
+      *tail_div = g_hints[i].tail_div;
       return g_hints[i].nseg;
+    }
   return 0;
 }
 
@@ -83,7 +90,9 @@ struct K2Plan {
   int ngroups = 0;   // bin groups of 4
   int nbp = 0;       // padded slab bins
   int nseg = 1;      // row segments per frame
-  int S = 0;         // rows per segment
+  int S = 0;         // rows per (big) segment
+  int nbig = 1;      // big segments; the rest are tail segments of S2 rows
+  int S2 = 0;
   int64_t Wp = 0;    // padded width = T * TW
   int T = 1;         // column tiles (colt)
   int TW = 0;        // tile width = nwarps * cpl * 128
@@ -97,6 +106,8 @@ struct K2Plan {
 };
 
 using K2Fn = void (*)(ih::ScanArgs, ih::RelLut);
+
+ih::Segs segs(const K2Plan& p) { return ih::Segs{p.S, p.nbig, p.S2}; }
 
 template <int CPL, int R, bool VEC, bool TMA, int MAXT>
 K2Fn pick_carry(int carry, bool colt) {
@@ -244,7 +255,8 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (nseg < 1) nseg = 1;
   p.slots = (int)slots;
   p.units = units;
-  const int32_t hinted = hint_lookup(frames, H, W, nb);
+  int32_t hinted_tail_pct = 0, hinted_tail_div = 0;
+  const int32_t hinted = hint_lookup(frames, H, W, nb, &hinted_tail_pct, &hinted_tail_div);
   if (hinted > 0) nseg = hinted < H ? hinted : H;
   const int64_t forced = env_int("IH_NSEG", 0);
   if (forced > 0) nseg = forced < H ? forced : H;
@@ -255,6 +267,24 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   p.S = (int)((H + nseg - 1) / nseg);
   if (nseg > 1 && p.S > 65535) p.S = 65535;
   p.nseg = (int)((H + p.S - 1) / p.S);
+  p.nbig = p.nseg;
+  p.S2 = p.S;
+  // tail split (IH_TAIL_PCT / hint): the last ~pct % of the rows become
+  // segments of S/div rows, dispatched last (segment-major scan grid)
+  int64_t tail_pct = env_int("IH_TAIL_PCT", hinted_tail_pct);
+  int64_t tail_div = env_int("IH_TAIL_DIV", hinted_tail_div > 0 ? hinted_tail_div : 4);
+  if (tail_pct > 0 && tail_pct < 100 && tail_div > 1 && p.nseg > 1 && H <= 65535) {
+    const int64_t s2 = (p.S + tail_div - 1) / tail_div;
+    const int64_t tail_rows = H * tail_pct / 100;
+    int64_t nbig = (H - tail_rows + p.S - 1) / p.S;  // big segments cover the rest
+    if (nbig < 1) nbig = 1;
+    if (nbig * p.S < H && s2 >= 8) {
+      const int64_t rem = H - nbig * p.S;
+      p.nbig = (int)nbig;
+      p.S2 = (int)s2;
+      p.nseg = (int)(nbig + (rem + s2 - 1) / s2);
+    }
+  }
   if (p.nseg <= 1) p.carry = ih::CARRY_NONE;
   else if (p.colt) p.carry = ih::CARRY_TABLE;
   else p.carry = env_int("IH_CARRY_LOOKBACK", 0) ? ih::CARRY_LOOKBACK : ih::CARRY_TABLE;
@@ -404,7 +434,7 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
             cudaSuccess)
       return cuda_fail("k2_colcounts_all smem attribute");
     if (launch(kern, grid, dim3(256), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
-               c.fstride, c.lut, p.S, p.nseg, p.nbp, p.Wp, (uint16_t*)ws, ctot) != cudaSuccess)
+               c.fstride, c.lut, segs(p), p.nseg, p.nbp, p.Wp, (uint16_t*)ws, ctot) != cudaSuccess)
       return cuda_fail("k2_colcounts_all");
     ++c.launched;
     return launch_colprefix(c, ws);
@@ -423,7 +453,7 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
           cudaSuccess)
     return cuda_fail("k2_colcounts smem attribute");
   if (launch(kern, grid, dim3(nw * 32), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
-             c.fstride, c.lut, p.S, p.nseg, p.nbp, p.Wp, nslab, (uint16_t*)ws, ctot) != cudaSuccess)
+             c.fstride, c.lut, segs(p), p.nseg, p.nbp, p.Wp, nslab, (uint16_t*)ws, ctot) != cudaSuccess)
     return cuda_fail("k2_colcounts");
   ++c.launched;
   return launch_colprefix(c, ws);
@@ -492,7 +522,7 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
   a.fstride = c.fstride;
   a.nb = c.nb;
   a.nbp = p.nbp;
-  a.S = p.S;
+  a.sg = segs(p);
   a.nseg = p.nseg;
   a.Wp = p.Wp;
   a.T = p.T;
@@ -514,7 +544,11 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
     a.lb_incl = a.lb_agg + lb_tiles(c.frames, p) * ih::kGroup * p.Wp;
   }
   a.out = out;
-  dim3 grid((unsigned)(p.ngroups * p.T), (unsigned)p.nseg, (unsigned)c.frames);
+  // segment-major: (units, frames, segments); look-back decodes its own ticket
+  dim3 grid((unsigned)(p.ngroups * p.T), (unsigned)c.frames, (unsigned)p.nseg);
+  if (p.carry == ih::CARRY_LOOKBACK)
+    grid = dim3((unsigned)(p.ngroups * p.T), (unsigned)p.nseg, (unsigned)c.frames);
+  a.trace = (g_trace && (size_t)grid.x * grid.y * grid.z <= g_trace_ctas) ? g_trace : nullptr;
   const int threads = p.nwarps * 32;
   return launch_k2(c, a, grid, threads);
 }
@@ -652,7 +686,7 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   const bool tma = aligned16 != 0 && env_int("IH_NO_TMA", 0) == 0;
   K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0, tma);
   const int k = resolve_kernel(kernel, p);
-  for (int i = 0; i < 12; ++i) info[i] = 0;
+  for (int i = 0; i < 14; ++i) info[i] = 0;
   info[0] = k;
   if (k == IH_KERNEL_CROSSWEAVE) {
     info[1] = height > 1 ? 2 : 1;
@@ -673,6 +707,8 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   info[9] = p.TW;
   info[10] = p.slots;
   info[11] = p.units;
+  info[12] = p.nbig;
+  info[13] = p.S2;
   return IH_OK;
 }
 
@@ -736,16 +772,20 @@ ih_status ih_likelihood_map_ws(const uint32_t* t, int32_t nb, int64_t height, in
 }
 
 ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
-                       int32_t nseg) {
+                       int32_t nseg, int32_t tail_pct, int32_t tail_div) {
   if (frames < 1 || height < 1 || width < 1) return fail(IH_ERR_SHAPE, "image must be non-empty");
   if (slab_bins < 1 || slab_bins > 256) return fail(IH_ERR_SHAPE, "bin count must be in [1, 256]");
   if (nseg < 0) return fail(IH_ERR_PARAM, "negative segment count");
+  if (tail_pct < 0 || tail_pct >= 100 || tail_div < 0)
+    return fail(IH_ERR_PARAM, "tail split must satisfy 0 <= pct < 100, div >= 0");
   std::lock_guard<std::mutex> lock(g_hint_mu);
   for (int i = 0; i < g_nhints; ++i) {
     PlanHint& h = g_hints[i];
     if (h.frames == frames && h.H == height && h.W == width && h.nb == slab_bins) {
       if (nseg > 0) {
         h.nseg = nseg;
+        h.tail_pct = tail_pct;
+        h.tail_div = tail_div;
       } else {
         h = g_hints[--g_nhints];
       }
@@ -754,8 +794,13 @@ ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t sl
   }
   if (nseg == 0) return IH_OK;
   if (g_nhints == kMaxHints) g_nhints = 0;  // a small cache: start over when full
-  g_hints[g_nhints++] = PlanHint{frames, height, width, slab_bins, nseg};
+  g_hints[g_nhints++] = PlanHint{frames, height, width, slab_bins, nseg, tail_pct, tail_div};
   return IH_OK;
+}
+
+void ih_debug_trace(void* device_buffer, size_t ctas) {
+  g_trace = (unsigned long long*)device_buffer;
+  g_trace_ctas = device_buffer ? ctas : 0;
 }
 
 const char* ih_status_string(ih_status s) {
@@ -772,6 +817,6 @@ const char* ih_status_string(ih_status s) {
 
 const char* ih_last_error(void) { return g_last_error; }
 
-int32_t ih_abi_version(void) { return (1 << 16) | 2; }
+int32_t ih_abi_version(void) { return (1 << 16) | 3; }
 
 }  // extern "C"

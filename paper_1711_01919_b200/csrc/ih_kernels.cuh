@@ -19,6 +19,16 @@ constexpr int kChunk = 128;       // columns per warp chunk
 constexpr int kGroup = 4;         // bins per packed group
 constexpr unsigned kFull = 0xffffffffu;
 
+// Row segmentation of a frame: `nbig` segments of S rows, then segments of S2
+// rows (S2 <= S: the short "tail" segments run last in the scan grid, which
+// shortens the end of the last wave).  Uniform when nbig == nseg.
+struct Segs {
+  int S, nbig, S2;
+  __host__ __device__ int64_t start(int64_t s) const {
+    return s < nbig ? s * S : (int64_t)nbig * S + (s - nbig) * S2;
+  }
+};
+
 // Per-call binning table: relative bin (lut[v] - bin_lo) or 0xFF when the
 // bin lies outside the slab [bin_lo, bin_hi).  Passed by value (kernel param).
 struct RelLut {

@@ -46,7 +46,7 @@ constexpr size_t kCountWarpSmem = (size_t)kCountRows * 4 * 32 * sizeof(uint16_t)
 template <bool ALIGNED, int kCountWarps>
 __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
-    RelLut lut, int S, int nseg, int nbp, int64_t Wp, int nslab, uint16_t* __restrict__ ws,
+    RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, int nslab, uint16_t* __restrict__ ws,
     uint32_t* __restrict__ ctot) {
   extern __shared__ __align__(16) uint16_t chist[];  // [warp][bin row][k][lane]
   __shared__ uint16_t sofs[512];  // pixel -> byte offset of its bin row (dummy row if none)
@@ -75,8 +75,8 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
   // this lane's counters: byte base + bin-row offset + k * 64
   char* hbase = reinterpret_cast<char*>(chist + (size_t)warp * kCountRows * 4 * 32 + lane);
   const uint8_t* base = img + f * fstride;
-  const int64_t seg0 = (int64_t)s * S;
-  const int64_t seg1 = (seg0 + S < H ? seg0 + S : H);
+  const int64_t seg0 = sg.start(s);
+  const int64_t seg1 = min(sg.start(s + 1), H);
   const int64_t per = (seg1 - seg0 + kCountWarps - 1) / kCountWarps;
   const int64_t r0 = seg0 + warp * per;
   const int64_t r1 = (r0 + per < seg1 ? r0 + per : seg1);
@@ -149,7 +149,7 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
 template <bool ALIGNED>
 __global__ void __launch_bounds__(256) k2_colcounts_all(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
-    RelLut lut, int S, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws,
+    RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws,
     uint32_t* __restrict__ ctot) {
   extern __shared__ __align__(16) uint32_t hist2[];  // [nbp][2][32]
   __shared__ uint32_t sw[512];  // pixel (| 256 past the edge) -> word offset of its bin, or ~0
@@ -174,8 +174,8 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
   __syncthreads();
   uint32_t* hl = hist2 + lane;
   const uint8_t* base = img + f * fstride;
-  const int64_t seg0 = (int64_t)s * S;
-  const int64_t seg1 = (seg0 + S < H ? seg0 + S : H);
+  const int64_t seg0 = sg.start(s);
+  const int64_t seg1 = min(sg.start(s + 1), H);
   auto load_px = [&](int64_t r) -> uint32_t {
     const uint8_t* row = base + r * pitch + c;
     if (ALIGNED) return __ldg(reinterpret_cast<const uint32_t*>(row));
@@ -354,7 +354,8 @@ struct ScanArgs {
   int64_t H, W, pitch, fstride;
   int nb;          // slab bins (bin_hi - bin_lo)
   int nbp;         // padded to a multiple of 4
-  int S, nseg;     // segment rows, segments per frame
+  Segs sg;         // row segmentation
+  int nseg;        // segments per frame
   int64_t Wp;      // padded width = T * TW (row stride of the carry tables)
   int T;           // column tiles per row (COLT kernels; 1 otherwise)
   int TW;          // tile width = warps * CPL * 128 = row stride of the smem ring
@@ -368,7 +369,14 @@ struct ScanArgs {
   uint32_t* lb_agg;        //   per-tile column counts      (ntiles, 4, Wp) u32
   uint32_t* lb_incl;       //   per-tile inclusive prefixes (ntiles, 4, Wp) u32
   uint32_t* out;
+  unsigned long long* trace;  // debug (ih_debug_trace): per CTA {start, prologue done, end, smid}
 };
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Row-segment carry schemes of k2_scan.
 enum Carry { CARRY_NONE = 0, CARRY_TABLE = 1, CARRY_LOOKBACK = 2 };
@@ -450,6 +458,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int64_t H = a.H, W = a.W;
+  const unsigned long long t_start = a.trace ? globaltimer() : 0ull;
 
   // Tile (frame f, bin group g, segment s).  With look-back carries the tile
   // comes from an atomic ticket, so every tile a CTA waits on has already
@@ -470,16 +479,18 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     } else {
       g = blockIdx.x;
     }
-    s = blockIdx.y;
-    f = blockIdx.z;
+    // segment-major grid: every frame's segment 0 first, the (short) tail
+    // segments last
+    s = blockIdx.z;
+    f = blockIdx.y;
   }
   const uint8_t* img = a.img + f * a.fstride;
   const int64_t ct = COLT ? (int64_t)t * a.TW : 0;  // first column of the tile
   // TMA bytes per row: the tile's columns rounded up to 16 (inside the pitched row)
   const uint32_t row_bytes =
       COLT ? (uint32_t)min((int64_t)a.TW, (W - ct + 15) / 16 * 16) : a.row_bytes;
-  const int64_t rs = (int64_t)s * a.S;
-  const int64_t re = (rs + a.S < H ? rs + a.S : H);
+  const int64_t rs = a.sg.start(s);
+  const int64_t re = min(a.sg.start(s + 1), H);
   const int nbatch = (int)((re - rs + R - 1) / R);
   // look-back: segments other than the last count their rows first (pass 0)
   const bool count_pass = CARRY == CARRY_LOOKBACK && s + 1 < a.nseg;
@@ -604,6 +615,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   }
 
   __syncthreads();  // oh[] and barriers ready
+  const unsigned long long t_ready = a.trace ? globaltimer() : 0ull;
 
   // 4 one-hot words of lane columns cl[k]..+3 for row rr of ring batch b
   auto onehot4 = [&](int b, int rr, int k, uint32_t o[4]) {
@@ -862,6 +874,18 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
           prow[k] += W;
         }
       }
+    }
+  }
+  if (a.trace) {  // debug timeline (uniform branch)
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      const size_t cta = blockIdx.x + (size_t)gridDim.x * (blockIdx.y + (size_t)gridDim.y * blockIdx.z);
+      a.trace[4 * cta + 0] = t_start;
+      a.trace[4 * cta + 1] = t_ready;
+      a.trace[4 * cta + 2] = globaltimer();
+      a.trace[4 * cta + 3] = smid;
     }
   }
 }

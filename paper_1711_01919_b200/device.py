@@ -102,7 +102,7 @@ def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel
 
 PLAN_FIELDS = ("kernel", "launches", "segments", "segment_rows", "chunks_per_lane",
                "rows_per_batch", "warps_per_cta", "workspace_bytes", "column_tiles", "tile_width",
-               "resident_ctas", "ctas_per_segment")
+               "resident_ctas", "ctas_per_segment", "big_segments", "tail_segment_rows")
 
 
 def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto",
@@ -116,9 +116,12 @@ def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "au
     return d
 
 
-def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments: int) -> None:
-    """Pin the row-segment count for one problem shape (0 removes the pin)."""
-    _native.check(_native.lib().ih_plan_hint(frames, height, width, slab_bins, int(segments)))
+def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments: int,
+                  tail_pct: int = 0, tail_div: int = 0) -> None:
+    """Pin the row-segment count (and optional tail split) for one problem
+    shape; segments = 0 removes the pin."""
+    _native.check(_native.lib().ih_plan_hint(frames, height, width, slab_bins, int(segments),
+                                             int(tail_pct), int(tail_div)))
 
 
 def segment_candidates(frames: int, height: int, width: int, slab_bins: int) -> list:
@@ -142,8 +145,10 @@ def segment_candidates(frames: int, height: int, width: int, slab_bins: int) -> 
 def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, device=None,
              candidates=None, reps: int = 5, images=None, out=None) -> dict:
     """Measure integral_histogram (prepare + scan, CUDA-graph replay) for each
-    candidate row-segment count on random frames of this shape, pin the fastest
-    with set_plan_hint, and return {"segments": best, "ms": {count: ms}}.
+    candidate row-segment count on random frames of this shape, then tail
+    splits (10/20/30 % of the rows in quarter-height segments run last) for the
+    best count; pin the fastest with set_plan_hint and return
+    {"segments", "tail_pct", "tail_div", "ms": {"count[/t<pct>]": ms}}.
     Results are bit-identical for every count; only the speed differs.
     ``images`` / ``out`` (CUDA tensors of the call's shapes) avoid allocating
     a second input and output."""
@@ -169,28 +174,40 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
     ws = torch.empty(need, dtype=torch.uint8, device=dev)
     side = torch.cuda.Stream(dev)
     times = {}
+
+    def measure(n, tail_pct=0, tail_div=0):
+        set_plan_hint(frames, height, width, nb, n, tail_pct, tail_div)
+        need = workspace_bytes(frames, height, width, nb)
+        w = ws if ws.numel() >= need else torch.empty(need, dtype=torch.uint8, device=dev)
+        for _ in range(2):  # warm: attributes, caches
+            integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=w)
+        torch.cuda.synchronize(dev)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=side):
+            integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=w)
+        g.replay()
+        e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        del g
+        return e0.elapsed_time(e1) / reps
+
     with torch.cuda.device(dev):
         for n in candidates:
-            set_plan_hint(frames, height, width, nb, n)
-            for _ in range(2):  # warm: attributes, caches
-                integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=ws)
-            torch.cuda.synchronize(dev)
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g, stream=side):
-                integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=ws)
-            g.replay()
-            e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
-            torch.cuda.synchronize(dev)
-            e0.record()
-            for _ in range(reps):
-                g.replay()
-            e1.record()
-            torch.cuda.synchronize(dev)
-            times[n] = e0.elapsed_time(e1) / reps
-            del g
+            times[(n, 0, 0)] = measure(n)
+        # second stage: short tail segments (run last) for the best count
+        n0 = min(times, key=times.get)[0]
+        if n0 > 1:
+            for tail_pct in (10, 20, 30):
+                times[(n0, tail_pct, 4)] = measure(n0, tail_pct, 4)
     best = min(times, key=times.get)
-    set_plan_hint(frames, height, width, nb, best)
-    return {"segments": best, "ms": {int(k): round(v, 4) for k, v in times.items()}}
+    set_plan_hint(frames, height, width, nb, *best)
+    return {"segments": best[0], "tail_pct": best[1], "tail_div": best[2],
+            "ms": {f"{k[0]}" + (f"/t{k[1]}" if k[1] else ""): round(v, 4) for k, v in times.items()}}
 
 
 def empty_output(frames: int, slab_bins: int, height: int, width: int, device) -> torch.Tensor:

@@ -1,0 +1,175 @@
+// Write-bandwidth probe: which store patterns reach the ~7.5 TB/s write-only
+// ceiling (memset) on B200, versus the K2 output pattern (CTA = 4 bin planes x
+// a segment of rows x full width, 16-byte evict-first stores).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ void st_cs(uint32_t* p, uint32_t a) {
+  asm volatile("st.global.cs.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p), "r"(a) : "memory");
+}
+__device__ __forceinline__ void st_wb(uint32_t* p, uint32_t a) {
+  asm volatile("st.global.v4.u32 [%0], {%1, %1, %1, %1};" ::"l"(p), "r"(a) : "memory");
+}
+
+__device__ __forceinline__ void st_v8(uint32_t* p, uint32_t a) {
+  asm volatile("st.global.v8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"l"(p), "r"(a) : "memory");
+}
+__global__ void linear_v8(uint32_t* out, size_t n32) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n32; i += (size_t)gridDim.x * blockDim.x)
+    st_v8(out + 8 * i, 7u);
+}
+// K2-like with 32-byte stores: lane owns 8 columns of NP planes
+template <int NP>
+__global__ void k2like_v8(uint32_t* out, int H, int W, int nb, int S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x, s = blockIdx.y, f = blockIdx.z;
+  const int64_t plane = (int64_t)H * W;
+  const int c = warp * 256 + lane * 8;
+  if (c >= W) return;
+  uint32_t* base = out + ((int64_t)f * nb + g * NP) * plane + c;
+  const int r0 = s * S, r1 = min(r0 + S, H);
+  for (int r = r0; r < r1; ++r) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) st_v8(base + i * plane + (int64_t)r * W, r);
+  }
+}
+// TMA bulk store: each CTA stages one row of NP planes in smem and bulk-copies
+// them out (thread 0 issues, bulk_group completion), double-buffered.
+template <int NP>
+__global__ void k2like_tma(uint32_t* out, int H, int W, int nb, int S) {
+  extern __shared__ __align__(128) uint32_t srow[];  // [2][NP][W]
+  const int g = blockIdx.x, s = blockIdx.y, f = blockIdx.z;
+  const int64_t plane = (int64_t)H * W;
+  uint32_t* base = out + ((int64_t)f * nb + g * NP) * plane;
+  const int r0 = s * S, r1 = min(r0 + S, H);
+  for (int r = r0; r < r1; ++r) {
+    uint32_t* buf = srow + ((r - r0) & 1) * NP * W;
+    if (threadIdx.x == 0)  // the buffer written 2 rows ago must have been read by the TMA
+      asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncthreads();
+    for (int i = threadIdx.x * 4; i < NP * W; i += blockDim.x * 4)
+      *reinterpret_cast<uint4*>(buf + i) = make_uint4(r, r, r, r);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < NP; ++i)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(base + i * plane + (int64_t)r * W),
+                     "r"((uint32_t)__cvta_generic_to_shared(buf + i * W)), "r"((uint32_t)(W * 4)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+// per-warp TMA bulk stores: each warp stages its 128 columns of NP planes for a
+// row (512 B per plane) and lane 0 bulk-copies them; NB buffers per warp
+template <int NP, int NB>
+__global__ void k2like_tma_warp(uint32_t* out, int H, int W, int nb, int S) {
+  extern __shared__ __align__(128) uint32_t sw[];  // [warp][NB][NP][128]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x, s = blockIdx.y, f = blockIdx.z;
+  const int64_t plane = (int64_t)H * W;
+  uint32_t* base = out + ((int64_t)f * nb + g * NP) * plane + warp * 128;
+  uint32_t* mine = sw + warp * NB * NP * 128;
+  const int r0 = s * S, r1 = min(r0 + S, H);
+  for (int r = r0; r < r1; ++r) {
+    uint32_t* buf = mine + ((r - r0) % NB) * NP * 128;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(NB - 1) : "memory");
+    __syncwarp();
+#pragma unroll
+    for (int i = 0; i < NP; ++i) *reinterpret_cast<uint4*>(buf + i * 128 + lane * 4) = make_uint4(r, r, r, r);
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+      for (int i = 0; i < NP; ++i)
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], 512;" ::"l"(base + i * plane + (int64_t)r * W),
+                     "r"((uint32_t)__cvta_generic_to_shared(buf + i * 128)) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+template <bool CS>
+__global__ void linear(uint32_t* out, size_t n16) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
+    CS ? st_cs(out + 4 * i, 7u) : st_wb(out + 4 * i, 7u);
+}
+
+// K2-like: grid (groups, segments, frames); 15 warps x 128 columns; per row,
+// each lane stores 16 B into each of NP planes (bins) of its group.
+template <bool CS, int NP>
+__global__ void k2like(uint32_t* out, int H, int W, int nb, int S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x, s = blockIdx.y, f = blockIdx.z;
+  const int64_t plane = (int64_t)H * W;
+  uint32_t* base = out + ((int64_t)f * nb + g * NP) * plane + warp * 128 + lane * 4;
+  const int r0 = s * S, r1 = min(r0 + S, H);
+  for (int r = r0; r < r1; ++r) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      uint32_t* p = base + i * plane + (int64_t)r * W;
+      CS ? st_cs(p, r) : st_wb(p, r);
+    }
+  }
+}
+
+int main() {
+  const int H = 1080, W = 1920, nb = 32, F = 64;
+  const size_t elems = (size_t)F * nb * H * W;
+  uint32_t* out;
+  cudaMalloc(&out, elems * 4);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto timeit = [&](const char* name, auto launch) {
+    launch();
+    cudaDeviceSynchronize();
+    cudaEventRecord(e0);
+    for (int i = 0; i < 5; ++i) launch();
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    ms /= 5;
+    printf("{\"probe\": \"%s\", \"ms\": %.4f, \"gbs\": %.1f}\n", name, ms, elems * 4 / ms / 1e6);
+  };
+  timeit("memset", [&] { cudaMemsetAsync(out, 0, elems * 4); });
+  timeit("linear_cs", [&] { linear<true><<<148 * 8, 256>>>(out, elems / 4); });
+  timeit("linear_wb", [&] { linear<false><<<148 * 8, 256>>>(out, elems / 4); });
+  timeit("linear_v8", [&] { linear_v8<<<148 * 8, 256>>>(out, elems / 8); });
+  for (int nseg : {5, 9}) {
+    const int S = (H + nseg - 1) / nseg;
+    char nm[64];
+    snprintf(nm, sizeof nm, "k2like_v8_np4_nseg%d", nseg);
+    timeit(nm, [&] { k2like_v8<4><<<dim3(nb / 4, nseg, F), 256>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "k2like_tma_np4_nseg%d", nseg);
+    cudaFuncSetAttribute(k2like_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * W * 4);
+    timeit(nm, [&] { k2like_tma<4><<<dim3(nb / 4, nseg, F), 480, 2 * 4 * W * 4>>>(out, H, W, nb, S); });
+  }
+  for (int nseg : {5, 9}) {
+    const int S = (H + nseg - 1) / nseg;
+    char nm[64];
+    snprintf(nm, sizeof nm, "k2like_tmawarp_nb2_nseg%d", nseg);
+    cudaFuncSetAttribute(k2like_tma_warp<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 15 * 2 * 4 * 512);
+    timeit(nm, [&] { k2like_tma_warp<4, 2><<<dim3(nb / 4, nseg, F), 480, 15 * 2 * 4 * 512>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "k2like_tmawarp_nb4_nseg%d", nseg);
+    cudaFuncSetAttribute(k2like_tma_warp<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 15 * 4 * 4 * 512);
+    timeit(nm, [&] { k2like_tma_warp<4, 4><<<dim3(nb / 4, nseg, F), 480, 15 * 4 * 4 * 512>>>(out, H, W, nb, S); });
+  }
+  for (int nseg : {3, 5, 9}) {
+    const int S = (H + nseg - 1) / nseg;
+    char nm[64];
+    snprintf(nm, sizeof nm, "k2like_cs_np4_nseg%d", nseg);
+    timeit(nm, [&] { k2like<true, 4><<<dim3(nb / 4, nseg, F), 480>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "k2like_wb_np4_nseg%d", nseg);
+    timeit(nm, [&] { k2like<false, 4><<<dim3(nb / 4, nseg, F), 480>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "k2like_cs_np1_nseg%d", nseg);
+    timeit(nm, [&] { k2like<true, 1><<<dim3(nb, nseg, F), 480>>>(out, H, W, nb, S); });
+  }
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+  return 0;
+}

@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_parity_gpu.py -q -x -k "likelihood or variants or window" > gpurun_out/pytest_k5.log 2>&1; echo pytest=$?
-(timeout 600 python scripts/bench_queries.py 2>&1 | grep "k5_"; IH_K5_DIRECT=1 timeout 600 python scripts/bench_queries.py 2>&1 | grep "k5_") > gpurun_out/queries_k5tab.jsonl
+timeout 900 python bench.py --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_w_hd64.json 2> gpurun_out/bench_w.err; echo b1=$?
+timeout 900 python bench.py --workload 8k256 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_w_8k256.json 2>> gpurun_out/bench_w.err
 echo done

@@ -35,7 +35,7 @@ for spec in sys.argv[1:]:
         k, v = part.split("=")
         combos = [dict(c, **{k: x}) for c in combos for x in v.split(",")]
     for c in combos:
-        for k in ("IH_NSEG", "IH_TARGET_WARPS", "IH_ROWS_PER_BATCH", "IH_MIN_SEG_ROWS", "IH_NO_TMA", "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE"):
+        for k in ("IH_NSEG", "IH_TARGET_WARPS", "IH_ROWS_PER_BATCH", "IH_MIN_SEG_ROWS", "IH_NO_TMA", "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_TAIL_PCT", "IH_TAIL_DIV"):
             os.environ.pop(k, None)
         os.environ.update(c)
         prep, scan, tot, frac, sfrac = timed(name)

@@ -26,7 +26,7 @@ def crc_of(t) -> str:
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
     for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
-              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT"):
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT", "IH_TAIL_PCT", "IH_TAIL_DIV"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -246,6 +246,31 @@ def test_colcounts_variants_256_bins(monkeypatch, rng, slab_counts):
             assert np.array_equal(got, full[lo:hi]), (h, w, bins, rng_)
 
 
+@pytest.mark.parametrize("tail", ["10:4", "30:2", "50:8"])
+@pytest.mark.parametrize("carry", ["table", "prefix", "lookback"])
+def test_tail_segments(monkeypatch, rng, tail, carry):
+    """Non-uniform row segmentation (big segments, then short tail segments
+    run last by the segment-major grid) under every carry scheme, with and
+    without column tiles and frame batches."""
+    pct, div = tail.split(":")
+    monkeypatch.setenv("IH_TAIL_PCT", pct)
+    monkeypatch.setenv("IH_TAIL_DIV", div)
+    monkeypatch.setenv("IH_NSEG", "6")
+    if carry == "prefix":
+        monkeypatch.setenv("IH_TABLE_SUM_MAX", "1")
+    elif carry == "lookback":
+        monkeypatch.setenv("IH_CARRY_LOOKBACK", "1")
+    for (F, h, w, bins) in [(1, 500, 700, 16), (3, 257, 300, 5), (1, 300, 4100, 32), (2, 130, 2500, 9)]:
+        frames = rng.integers(0, 256, (F, h, w), dtype=np.uint8)
+        lut = O.np_uniform_table(bins)
+        p = device.plan(F, h, w, bins)
+        assert p["segments"] >= 6
+        got = device.integral_histogram(torch.from_numpy(frames).cuda(), lut, bins,
+                                        kernel="single_pass").cpu().numpy()
+        for f in range(F):
+            assert np.array_equal(got[f], O.compute_crossweave(frames[f], lut, bins)), (F, h, w, bins, f)
+
+
 def test_column_tiles_unaligned_slabs_and_frames(rng):
     """Column tiles with an odd pitch / byte offset (LDG rows), bin slabs and a
     frame batch; constant columns stress the row-carry atomics."""
@@ -422,8 +447,10 @@ def test_autotune_pins_a_measured_segment_count(rng):
     the pinned plan still produces the oracle's tensor."""
     res = device.autotune(3, 300, 700, 12)
     try:
-        assert res["segments"] in res["ms"] and len(res["ms"]) >= 1
-        assert device.plan(3, 300, 700, 12)["segments"] == res["segments"]
+        assert str(res["segments"]) in {k.split("/")[0] for k in res["ms"]}
+        p = device.plan(3, 300, 700, 12)
+        assert p["segments"] >= res["segments"]
+        assert (p["big_segments"] < p["segments"]) == (res["tail_pct"] > 0)
         frames = rng.integers(0, 256, (3, 300, 700), dtype=np.uint8)
         t = ih.compute_frames(frames, ih.BinSpec.uniform(12))
         for f in range(3):
