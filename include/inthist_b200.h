@@ -116,11 +116,14 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
  * ih_integral_histogram then splits each frame into `nseg` row segments
  * instead of its heuristic choice; with tail_pct > 0 the last ~tail_pct % of
  * the rows become short segments of 1/tail_div the height (0: 4), which the
- * segment-major scan grid runs last.  Results are identical for every choice;
- * only speed changes.  nseg = 0 removes the hint.  A small process-wide table
- * guarded by a mutex; device.autotune() fills it from measurements. */
+ * segment-major scan grid runs last.  flags bit 0: carry the segments through
+ * a thread-block cluster (the <= 16 segments of a strip exchange their column
+ * counts in distributed shared memory: one launch, no prepass; taken when the
+ * plan allows it -- no column tiles, H < 65536).  Results are identical for
+ * every choice; only speed changes.  nseg = 0 removes the hint.  A small
+ * process-wide table guarded by a mutex; device.autotune() fills it. */
 ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
-                       int32_t nseg, int32_t tail_pct, int32_t tail_div);
+                       int32_t nseg, int32_t tail_pct, int32_t tail_div, int32_t flags);
 
 /* Batched four-corner region queries (core.py:179-195).
  *   t        device (nb, height, width) uint32 integral histogram (a slab is fine)

@@ -87,7 +87,7 @@ def lib() -> ctypes.CDLL:
     L.ih_likelihood_workspace_bytes.restype = ctypes.c_size_t
     L.ih_plan_describe.argtypes = [i64, i64, i64, i32, i32, i32, P]
     L.ih_plan_describe.restype = ctypes.c_int
-    L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32, i32, i32]
+    L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32, i32, i32, i32]
     L.ih_plan_hint.restype = ctypes.c_int
     L.ih_status_string.argtypes = [ctypes.c_int]
     L.ih_status_string.restype = ctypes.c_char_p

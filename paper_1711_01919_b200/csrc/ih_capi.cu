@@ -41,8 +41,9 @@ constexpr int kNumSMs = 148;
 // set by an autotuner; consulted by plan_k2 before its own heuristic.
 struct PlanHint {
   int64_t frames, H, W;
-  int32_t nb, nseg, tail_pct, tail_div;
+  int32_t nb, nseg, tail_pct, tail_div, flags;
 };
+constexpr int32_t kHintCluster = 1;  // ih_plan_hint flags: cluster (DSMEM) carries
 constexpr int kMaxHints = 64;
 PlanHint g_hints[kMaxHints];
 int g_nhints = 0;
@@ -52,12 +53,13 @@ unsigned long long* g_trace = nullptr;  // ih_debug_trace
 size_t g_trace_ctas = 0;
 
 int32_t hint_lookup(int64_t frames, int64_t H, int64_t W, int32_t nb, int32_t* tail_pct,
-                    int32_t* tail_div) {
+                    int32_t* tail_div, int32_t* flags) {
   std::lock_guard<std::mutex> lock(g_hint_mu);
   for (int i = 0; i < g_nhints; ++i)
     if (g_hints[i].frames == frames && g_hints[i].H == H && g_hints[i].W == W && g_hints[i].nb == nb) {
       *tail_pct = g_hints[i].tail_pct;
       *tail_div = g_hints[i].tail_div;
+      *flags = g_hints[i].flags;
       return g_hints[i].nseg;
     }
   return 0;
@@ -119,6 +121,10 @@ K2Fn pick_carry(int carry, bool colt) {
   }
   if (colt) return nullptr;
   switch (carry) {
+    case ih::CARRY_CLUSTER:
+      if constexpr (MAXT == 512 && CPL == 1)
+        return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_CLUSTER, MAXT, false>;
+      return nullptr;
     case ih::CARRY_TABLE: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_TABLE, MAXT, false>;
     case ih::CARRY_LOOKBACK: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_LOOKBACK, MAXT, false>;
     default: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_NONE, MAXT, false>;
@@ -255,8 +261,9 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (nseg < 1) nseg = 1;
   p.slots = (int)slots;
   p.units = units;
-  int32_t hinted_tail_pct = 0, hinted_tail_div = 0;
-  const int32_t hinted = hint_lookup(frames, H, W, nb, &hinted_tail_pct, &hinted_tail_div);
+  int32_t hinted_tail_pct = 0, hinted_tail_div = 0, hinted_flags = 0;
+  const int32_t hinted =
+      hint_lookup(frames, H, W, nb, &hinted_tail_pct, &hinted_tail_div, &hinted_flags);
   if (hinted > 0) nseg = hinted < H ? hinted : H;
   const int64_t forced = env_int("IH_NSEG", 0);
   if (forced > 0) nseg = forced < H ? forced : H;
@@ -285,7 +292,13 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
       p.nseg = (int)(nbig + (rem + s2 - 1) / s2);
     }
   }
+  // cluster carries: the segments of a strip are one thread-block cluster
+  // (<= 16 CTAs) exchanging counts through distributed shared memory -- one
+  // launch, no prepass; CPL-1 512-thread kernels without column tiles, H < 65536
+  const bool cluster_ok = !p.colt && !p.big && p.cpl == 1 && p.nseg <= 16 && H <= 65535;
+  const bool want_cluster = env_int("IH_CARRY_CLUSTER", (hinted_flags & kHintCluster) ? 1 : 0) != 0;
   if (p.nseg <= 1) p.carry = ih::CARRY_NONE;
+  else if (want_cluster && cluster_ok) p.carry = ih::CARRY_CLUSTER;
   else if (p.colt) p.carry = ih::CARRY_TABLE;
   else p.carry = env_int("IH_CARRY_LOOKBACK", 0) ? ih::CARRY_LOOKBACK : ih::CARRY_TABLE;
   return p;
@@ -482,8 +495,26 @@ ih_status launch_k2(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads
     return cuda_fail("k2_scan smem attribute");
   // look-back carries read flags a memset just reset: never PDL there
   const bool pdl = c.pdl() && c.plan.carry != ih::CARRY_LOOKBACK;
-  if (launch(fn, grid, dim3(threads), smem, c.stream, pdl, a, c.lut) != cudaSuccess)
+  if (c.plan.carry == ih::CARRY_CLUSTER) {  // cluster = the segments of one strip
+    if (c.plan.nseg > 8 &&
+        cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1) != cudaSuccess)
+      return cuda_fail("k2_scan cluster size attribute");
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 1;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = (unsigned)c.plan.nseg;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaLaunchKernelEx(&cfg, fn, a, c.lut) != cudaSuccess) return cuda_fail("k2_scan (cluster)");
+  } else if (launch(fn, grid, dim3(threads), smem, c.stream, pdl, a, c.lut) != cudaSuccess) {
     return cuda_fail("k2_scan");
+  }
   ++c.launched;
   return IH_OK;
 }
@@ -772,7 +803,7 @@ ih_status ih_likelihood_map_ws(const uint32_t* t, int32_t nb, int64_t height, in
 }
 
 ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
-                       int32_t nseg, int32_t tail_pct, int32_t tail_div) {
+                       int32_t nseg, int32_t tail_pct, int32_t tail_div, int32_t flags) {
   if (frames < 1 || height < 1 || width < 1) return fail(IH_ERR_SHAPE, "image must be non-empty");
   if (slab_bins < 1 || slab_bins > 256) return fail(IH_ERR_SHAPE, "bin count must be in [1, 256]");
   if (nseg < 0) return fail(IH_ERR_PARAM, "negative segment count");
@@ -786,6 +817,7 @@ ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t sl
         h.nseg = nseg;
         h.tail_pct = tail_pct;
         h.tail_div = tail_div;
+        h.flags = flags;
       } else {
         h = g_hints[--g_nhints];
       }
@@ -794,7 +826,7 @@ ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t sl
   }
   if (nseg == 0) return IH_OK;
   if (g_nhints == kMaxHints) g_nhints = 0;  // a small cache: start over when full
-  g_hints[g_nhints++] = PlanHint{frames, height, width, slab_bins, nseg, tail_pct, tail_div};
+  g_hints[g_nhints++] = PlanHint{frames, height, width, slab_bins, nseg, tail_pct, tail_div, flags};
   return IH_OK;
 }
 

@@ -378,8 +378,28 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 
+__device__ __forceinline__ uint32_t smem_u32_any(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
 // Row-segment carry schemes of k2_scan.
-enum Carry { CARRY_NONE = 0, CARRY_TABLE = 1, CARRY_LOOKBACK = 2 };
+enum Carry { CARRY_NONE = 0, CARRY_TABLE = 1, CARRY_LOOKBACK = 2, CARRY_CLUSTER = 3 };
+
+// Thread-block-cluster helpers (CARRY_CLUSTER): the segments of one strip form
+// one cluster; counts are exchanged through distributed shared memory.
+__device__ __forceinline__ void cluster_arrive_release() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait_acquire() {
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// load a u32 from the same shared-memory offset in cluster CTA `rank`
+__device__ __forceinline__ uint32_t ld_dsmem(const uint32_t* local, uint32_t rank) {
+  uint32_t remote, v;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32_any(local)), "r"(rank));
+  asm volatile("ld.shared::cluster.u32 %0, [%1];" : "=r"(v) : "r"(remote) : "memory");
+  return v;
+}
 constexpr uint32_t kFlagAgg = 1u, kFlagIncl = 2u;
 
 __device__ __forceinline__ uint32_t ld_acquire_gpu(const uint32_t* p) {
@@ -447,6 +467,11 @@ template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT, bool COLT>
 __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut lut) {
   constexpr int NST = Ring<R>::kStages;
   static_assert(!(COLT && CARRY == CARRY_LOOKBACK), "column tiles use table carries");
+  static_assert(!(COLT && CARRY == CARRY_CLUSTER), "column tiles use table carries");
+  constexpr bool CL = CARRY == CARRY_CLUSTER;
+  // CARRY_CLUSTER: this CTA's per-column segment counts, [word][thread]
+  // (word = (k*4 + j)*2 + {0: bins 0/2, 1: bins 1/3}, 16-bit lanes)
+  __shared__ uint32_t ccnt[CL && CPL == 1 ? 8 * 512 : 1];
   __shared__ uint32_t oh[kOneHotEntries];
   __shared__ uint4 tot[2][R][32];
   __shared__ uint4 sleft[2][COLT ? R : 1];  // COLT: per-row counts left of the tile
@@ -493,7 +518,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   const int64_t re = min(a.sg.start(s + 1), H);
   const int nbatch = (int)((re - rs + R - 1) / R);
   // look-back: segments other than the last count their rows first (pass 0)
-  const bool count_pass = CARRY == CARRY_LOOKBACK && s + 1 < a.nseg;
+  const bool count_pass = (CARRY == CARRY_LOOKBACK || CL) && s + 1 < a.nseg;
   const int nb_count = count_pass ? nbatch : 0;
   const int nb_total = nb_count + nbatch;
 
@@ -629,6 +654,64 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
       load_onehot4<false>(img + (batch_row0(b) + rr) * a.pitch, ct + cl[k], W, oh, inval[k], o);
     }
   };
+
+  if (CL) {
+    // ---- pass 0 (all but the last segment): per-column counts of this
+    // segment's rows, 4 bins in two words of 16-bit lanes, into ccnt[]
+    if (count_pass) {
+      uint32_t ce[CPL][4], co[CPL][4];
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) ce[k][j] = co[k][j] = 0u;
+      for (int b = 0; b < nb_count; ++b) {
+        const int rows = (int)(re - batch_row0(b) < R ? re - batch_row0(b) : R);
+        if (TMA) mbar_wait(&full_bar[b % NST], (uint32_t)((b / NST) & 1));
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          if (rr < rows) {
+#pragma unroll
+            for (int k = 0; k < CPL; ++k) {
+              uint32_t o[4];
+              onehot4(b, rr, k, o);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                ce[k][j] += o[j] & 0x00ff00ffu;
+                co[k][j] += (o[j] >> 8) & 0x00ff00ffu;
+              }
+            }
+          }
+        }
+        __syncthreads();  // ring stage consumed
+        if (TMA && threadIdx.x == 0 && b + NST < nb_total) issue(b + NST);
+      }
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          ccnt[((k * 4 + j) * 2 + 0) * blockDim.x + threadIdx.x] = ce[k][j];
+          ccnt[((k * 4 + j) * 2 + 1) * blockDim.x + threadIdx.x] = co[k][j];
+        }
+    }
+    cluster_arrive_release();  // counts visible cluster-wide
+    cluster_wait_acquire();
+    // ---- carry: sum the counts of the cluster's segments above (DSMEM reads;
+    // cluster rank = segment, every column sum < 65536 since H < 65536)
+    for (int sp = 0; sp < s; ++sp) {
+#pragma unroll
+      for (int k = 0; k < CPL; ++k)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const uint32_t e = ld_dsmem(&ccnt[((k * 4 + j) * 2 + 0) * blockDim.x + threadIdx.x], sp);
+          const uint32_t o = ld_dsmem(&ccnt[((k * 4 + j) * 2 + 1) * blockDim.x + threadIdx.x], sp);
+          acc[k][j][0] += e & 0xffffu;
+          acc[k][j][1] += o & 0xffffu;
+          acc[k][j][2] += e >> 16;
+          acc[k][j][3] += o >> 16;
+        }
+    }
+    cluster_arrive_release();  // done reading the others' ccnt (waited at exit)
+  }
 
   if (CARRY == CARRY_LOOKBACK) {
     const int64_t ntile_vec = (int64_t)kGroup * a.Wp;  // u32 per published vector
@@ -876,6 +959,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
       }
     }
   }
+  if (CL) cluster_wait_acquire();  // no CTA leaves while a neighbour may read its ccnt[]
   if (a.trace) {  // debug timeline (uniform branch)
     __syncthreads();
     if (threadIdx.x == 0) {

@@ -117,11 +117,11 @@ def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "au
 
 
 def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments: int,
-                  tail_pct: int = 0, tail_div: int = 0) -> None:
-    """Pin the row-segment count (and optional tail split) for one problem
-    shape; segments = 0 removes the pin."""
+                  tail_pct: int = 0, tail_div: int = 0, cluster: bool = False) -> None:
+    """Pin the row-segment count (optional tail split, optional cluster/DSMEM
+    carries) for one problem shape; segments = 0 removes the pin."""
     _native.check(_native.lib().ih_plan_hint(frames, height, width, slab_bins, int(segments),
-                                             int(tail_pct), int(tail_div)))
+                                             int(tail_pct), int(tail_div), 1 if cluster else 0))
 
 
 def segment_candidates(frames: int, height: int, width: int, slab_bins: int) -> list:

@@ -92,6 +92,23 @@ __global__ void k2like_tma_warp(uint32_t* out, int H, int W, int nb, int S) {
   if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// K2-like, batches of RB rows written plane by plane (bin-outer, row-inner)
+template <int NP, int RB>
+__global__ void k2like_planeorder(uint32_t* out, int H, int W, int nb, int S) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = blockIdx.x, s = blockIdx.y, f = blockIdx.z;
+  const int64_t plane = (int64_t)H * W;
+  uint32_t* base = out + ((int64_t)f * nb + g * NP) * plane + warp * 128 + lane * 4;
+  const int r0 = s * S, r1 = min(r0 + S, H);
+  for (int r = r0; r < r1; r += RB) {
+#pragma unroll
+    for (int i = 0; i < NP; ++i)
+#pragma unroll
+      for (int rr = 0; rr < RB; ++rr)
+        if (r + rr < r1) st_cs(base + i * plane + (int64_t)(r + rr) * W, r);
+  }
+}
+
 template <bool CS>
 __global__ void linear(uint32_t* out, size_t n16) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n16; i += (size_t)gridDim.x * blockDim.x)
@@ -158,6 +175,14 @@ int main() {
     snprintf(nm, sizeof nm, "k2like_tmawarp_nb4_nseg%d", nseg);
     cudaFuncSetAttribute(k2like_tma_warp<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 15 * 4 * 4 * 512);
     timeit(nm, [&] { k2like_tma_warp<4, 4><<<dim3(nb / 4, nseg, F), 480, 15 * 4 * 4 * 512>>>(out, H, W, nb, S); });
+  }
+  for (int nseg : {5, 9}) {
+    const int S = (H + nseg - 1) / nseg;
+    char nm[64];
+    snprintf(nm, sizeof nm, "k2like_planeorder_rb4_nseg%d", nseg);
+    timeit(nm, [&] { k2like_planeorder<4, 4><<<dim3(nb / 4, nseg, F), 480>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "k2like_planeorder_rb8_nseg%d", nseg);
+    timeit(nm, [&] { k2like_planeorder<4, 8><<<dim3(nb / 4, nseg, F), 480>>>(out, H, W, nb, S); });
   }
   for (int nseg : {3, 5, 9}) {
     const int S = (H + nseg - 1) / nseg;

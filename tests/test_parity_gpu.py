@@ -26,7 +26,7 @@ def crc_of(t) -> str:
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
     for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
-              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT", "IH_TAIL_PCT", "IH_TAIL_DIV"):
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_CLUSTER"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -99,7 +99,7 @@ SHAPES = [(1, 1), (1, 193), (193, 1), (7, 131), (61, 257), (128, 128), (96, 500)
 @pytest.mark.parametrize("nseg", [0, 2, 3, 7])
 @pytest.mark.parametrize("rows_per_batch", [1, 2, 4])
 @pytest.mark.parametrize("tma", [True, False])
-@pytest.mark.parametrize("carry", ["lookback", "table_sum", "table_prefix"])
+@pytest.mark.parametrize("carry", ["lookback", "table_sum", "table_prefix", "cluster"])
 def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch, tma, carry):
     """Force K2 row segmentation (colcounts/colprefix/carry-init path), every
     barrier batch size, and both input paths (TMA smem ring / LDG); compare
@@ -113,6 +113,8 @@ def test_segments_and_batches(monkeypatch, rng, nseg, rows_per_batch, tma, carry
         monkeypatch.setenv("IH_CARRY_LOOKBACK", "1")
     elif carry == "table_prefix":
         monkeypatch.setenv("IH_TABLE_SUM_MAX", "1")  # always run k2_colprefix
+    elif carry == "cluster":
+        monkeypatch.setenv("IH_CARRY_CLUSTER", "1")  # DSMEM carries where the plan allows
     for (h, w) in SHAPES:
         bins = int(rng.choice([1, 3, 5, 16, 64]))
         px = rng.integers(0, 256, (h, w), dtype=np.uint8)
@@ -247,7 +249,7 @@ def test_colcounts_variants_256_bins(monkeypatch, rng, slab_counts):
 
 
 @pytest.mark.parametrize("tail", ["10:4", "30:2", "50:8"])
-@pytest.mark.parametrize("carry", ["table", "prefix", "lookback"])
+@pytest.mark.parametrize("carry", ["table", "prefix", "lookback", "cluster"])
 def test_tail_segments(monkeypatch, rng, tail, carry):
     """Non-uniform row segmentation (big segments, then short tail segments
     run last by the segment-major grid) under every carry scheme, with and
@@ -260,6 +262,8 @@ def test_tail_segments(monkeypatch, rng, tail, carry):
         monkeypatch.setenv("IH_TABLE_SUM_MAX", "1")
     elif carry == "lookback":
         monkeypatch.setenv("IH_CARRY_LOOKBACK", "1")
+    elif carry == "cluster":
+        monkeypatch.setenv("IH_CARRY_CLUSTER", "1")
     for (F, h, w, bins) in [(1, 500, 700, 16), (3, 257, 300, 5), (1, 300, 4100, 32), (2, 130, 2500, 9)]:
         frames = rng.integers(0, 256, (F, h, w), dtype=np.uint8)
         lut = O.np_uniform_table(bins)
@@ -552,3 +556,28 @@ def test_frame_pipeline_host_to_host(rng, piece_bytes):
         for f in range(5):
             want = O.compute_crossweave(frames[f], spec.table, 11)[2:9]
             assert np.array_equal(h_out[f].numpy(), want)
+
+
+@pytest.mark.parametrize("nseg", [2, 5, 8, 9, 16])
+def test_cluster_carries(monkeypatch, rng, nseg):
+    """CARRY_CLUSTER: the segments of a strip form one thread-block cluster
+    (up to 16 CTAs, non-portable above 8) and read their neighbours' column
+    counts from distributed shared memory; frame batches, bin slabs, 256 bins,
+    unaligned rows."""
+    monkeypatch.setenv("IH_CARRY_CLUSTER", "1")
+    monkeypatch.setenv("IH_NSEG", str(nseg))
+    for (F, h, w, bins, rng_) in [(1, 512, 512, 32, None), (3, 300, 1000, 7, None),
+                                  (1, 200, 2048, 256, (5, 200)), (2, 999, 130, 16, None)]:
+        frames = rng.integers(0, 256, (F, h, w), dtype=np.uint8)
+        lut = O.np_uniform_table(bins)
+        p = device.plan(F, h, w, bins if rng_ is None else rng_[1] - rng_[0])
+        assert p["launches"] == 1, p  # no prepass
+        got = device.integral_histogram(torch.from_numpy(frames).cuda(), lut, bins, bin_range=rng_,
+                                        kernel="single_pass").cpu().numpy()
+        lo, hi = rng_ or (0, bins)
+        for f in range(F):
+            assert np.array_equal(got[f], O.compute_crossweave(frames[f], lut, bins)[lo:hi]), (F, h, w, f)
+    base = rng.integers(0, 256, (77, 333 + 3), dtype=np.uint8)
+    view = torch.from_numpy(base).cuda()[:, 3:]
+    got = device.integral_histogram(view, O.np_uniform_table(9), 9, kernel="single_pass").cpu().numpy()
+    assert np.array_equal(got, O.compute_crossweave(np.ascontiguousarray(base[:, 3:]), O.np_uniform_table(9), 9))
