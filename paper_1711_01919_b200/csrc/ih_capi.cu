@@ -675,14 +675,22 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   const int64_t k4mode = env_int("IH_K4_MODE", 1);  // 0 corners, 1 ILP corners, 2 staged
   if (k4mode == 1) {
     // rows are grid-strided over ~64 CTAs per SM in total, so each CTA walks
-    // several rows (one-row CTAs: 0.52 of HBM, 148*64 CTAs: 0.59, HD x32)
+    // several rows (one-row CTAs: 0.52 of HBM, 148*64 CTAs: 0.59, HD x32;
+    // with u32 window arithmetic and <= 40 registers: 0.70)
     const int64_t cb = (C + 1023) / 1024;
     int64_t ry = (int64_t)kNumSMs * 64 / (cb * nb);
     ry = ry < 1 ? 1 : ry > R ? R : ry > 65535 ? 65535 : ry;
     ry = env_int("IH_K4_ROWS_GRID", ry);
     dim3 grid((unsigned)cb, (unsigned)ry, (unsigned)nb);
-    ih::k4_window_counts_ilp<4><<<grid, 256, 0, (cudaStream_t)stream>>>(
-        t, nb, height, width, h, w, reinterpret_cast<long long*>(out));
+    // IH_K4_VARIANT = U*10 + min CTAs/SM (A/B; 46 measured best, profiles/r01f/queries_k4_variants.jsonl)
+    const int64_t v = env_int("IH_K4_VARIANT", 46);
+    auto k = v == 48 ? ih::k4_window_counts_ilp<4, 8> : v == 28 ? ih::k4_window_counts_ilp<2, 8>
+           : v == 86 ? ih::k4_window_counts_ilp<8, 6> : v == 84 ? ih::k4_window_counts_ilp<8, 4>
+                     : ih::k4_window_counts_ilp<4, 6>;
+    const int U = v / 10 == 2 ? 2 : v / 10 == 8 ? 8 : 4;
+    grid.x = (unsigned)((C + 256 * U - 1) / (256 * U));
+    k<<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h, w,
+                                            reinterpret_cast<long long*>(out));
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts_ilp");
     return IH_OK;
   }

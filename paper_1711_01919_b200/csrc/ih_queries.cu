@@ -83,8 +83,8 @@ __global__ void __launch_bounds__(256) k4_window_counts(const uint32_t* __restri
 // K4 (ILP): as k4_window_counts with U outputs per thread (columns j + u*256),
 // all 4U corner loads issued before the first store: the corner reads are L2
 // hits, so memory-level parallelism per thread decides the throughput.
-template <int U>
-__global__ void __launch_bounds__(256) k4_window_counts_ilp(const uint32_t* __restrict__ t, int nb,
+template <int U, int MINB>
+__global__ void __launch_bounds__(256, MINB) k4_window_counts_ilp(const uint32_t* __restrict__ t, int nb,
                                                              int64_t H, int64_t W, int h, int w,
                                                              long long* __restrict__ out) {
   const int64_t R = H - h + 1, C = W - w + 1;
@@ -107,9 +107,9 @@ __global__ void __launch_bounds__(256) k4_window_counts_ilp(const uint32_t* __re
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t j = ((int64_t)blockIdx.x * U + u) * blockDim.x + threadIdx.x;
-      if (j < C)
-        __stcs(orow + j, (long long)a[u][0] - (long long)a[u][1] - (long long)a[u][2] +
-                             (long long)a[u][3]);
+      // the window count is exact in u32 (0 <= n <= h*w < 2^32): modular
+      // arithmetic, then a zero-extending store
+      if (j < C) __stcs(orow + j, (long long)(a[u][0] - a[u][1] - a[u][2] + a[u][3]));
     }
   }
 }
