@@ -130,8 +130,21 @@ def compute_wavefront(img: GrayImage, spec: BinSpec, tile: int = DEFAULT_TILE,
     return ih
 
 
-def compute(img: GrayImage, spec: BinSpec, strategy: Strategy, workers: int = 0) -> IntegralHistogram:
-    """Dispatch by strategy name (strategies.py:219-229); results never differ."""
+def compute(img: GrayImage, spec: BinSpec, strategy: Strategy, workers: int = 0,
+            devices=None) -> IntegralHistogram:
+    """Dispatch by strategy name (strategies.py:219-229); results never differ.
+
+    ``devices`` (an extension; the reference has no such argument): a list of
+    CUDA devices over which the bins are sharded (the paper's multi-GPU
+    decomposition, multi.integral_histogram_devices); the result is the same
+    host tensor."""
+    if devices is not None:
+        from . import multi
+
+        resolve_workers(workers)
+        counts = multi.integral_histogram_devices(img.pixels, spec.table, spec.bins, devices,
+                                                  shard="bins", out="host")
+        return IntegralHistogram(counts[0])
     name = strategy.name
     if name == "wavefront":
         return compute_wavefront(img, spec, strategy.tile, workers)
@@ -142,11 +155,24 @@ def compute(img: GrayImage, spec: BinSpec, strategy: Strategy, workers: int = 0)
     return compute_sequential(img, spec)
 
 
-def compute_frames(frames, spec: BinSpec, bin_range=None, kernel: str = "auto"):
+def compute_frames(frames, spec: BinSpec, bin_range=None, kernel: str = "auto", devices=None,
+                   shard: str = "frames"):
     """Batched video path (no reference equivalent; the reference takes one
     GrayImage per call): (F, H, W) uint8 host or CUDA frames -> CUDA tensor
-    (F, B, H, W) uint32, or the bins [lo, hi) of ``bin_range``."""
+    (F, B, H, W) uint32, or the bins [lo, hi) of ``bin_range``.
+
+    With ``devices`` (host frames), the frames (``shard="frames"``) or the bins
+    (``shard="bins"``) are split over those devices and the result is
+    assembled on ``devices[0]`` by peer copies."""
     import torch
+
+    if devices is not None:
+        from . import multi
+
+        if bin_range is not None:
+            raise ParameterError("bin_range and devices= cannot be combined")
+        return multi.integral_histogram_devices(frames, spec.table, spec.bins, devices,
+                                                shard=shard, out="device")
 
     if isinstance(frames, np.ndarray):
         frames = torch.from_numpy(np.ascontiguousarray(frames, dtype=np.uint8))

@@ -581,3 +581,33 @@ def test_cluster_carries(monkeypatch, rng, nseg):
     view = torch.from_numpy(base).cuda()[:, 3:]
     got = device.integral_histogram(view, O.np_uniform_table(9), 9, kernel="single_pass").cpu().numpy()
     assert np.array_equal(got, O.compute_crossweave(np.ascontiguousarray(base[:, 3:]), O.np_uniform_table(9), 9))
+
+
+@pytest.mark.parametrize("shard", ["bins", "frames"])
+@pytest.mark.parametrize("out", ["host", "device", "shards"])
+def test_devices_kwarg_single_process(rng, shard, out):
+    """multi.integral_histogram_devices (the devices= form): shards over a
+    device list (here the one GPU three times, separate streams), every output
+    mode, equal to the oracle; compute(..., devices=) and
+    compute_frames(..., devices=) use it."""
+    from paper_1711_01919_b200 import multi
+
+    frames = rng.integers(0, 256, (4, 90, 300), dtype=np.uint8)
+    lut = O.np_uniform_table(11)
+    want = np.stack([O.compute_crossweave(f, lut, 11) for f in frames])
+    res = multi.integral_histogram_devices(frames, lut, 11, [0, 0, 0], shard=shard, out=out)
+    if out == "host":
+        got = res
+    elif out == "device":
+        got = res.cpu().numpy()
+    else:
+        got = np.zeros_like(want)
+        for (f0, f1, b0, b1), t in res:
+            if t is not None:
+                got[f0:f1, b0:b1] = t.cpu().numpy()
+    assert np.array_equal(got, want)
+    img = ih.GrayImage(frames[0])
+    assert np.array_equal(ih.compute(img, ih.BinSpec.uniform(11), ih.SEQUENTIAL, devices=[0, 0]).counts,
+                          want[0])
+    t = ih.compute_frames(frames, ih.BinSpec.uniform(11), devices=[0, 0], shard=shard)
+    assert np.array_equal(t.cpu().numpy(), want)
