@@ -105,9 +105,7 @@ def integral_histogram_devices(images, table, bins: int, devices, shard: str = "
             rs.wait_event(ev)
             with torch.cuda.stream(rs):
                 full[f0:f1, b0:b1].copy_(part, non_blocking=True)  # peer copy across devices
-                if part.device != full.device:
-                    part.record_stream(rs)
-        torch.cuda.synchronize(devs[root])
+        torch.cuda.synchronize(devs[root])  # copies done before the parts are freed
         return full
     for d, s, ev, *_ in events:
         ev.synchronize()
