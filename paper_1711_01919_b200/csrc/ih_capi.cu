@@ -7,6 +7,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <utility>
 
 #include "../../include/inthist_b200.h"
@@ -107,6 +108,23 @@ struct K2Plan {
   bool tma = true;   // 16-byte aligned rows
 };
 
+// Opt a kernel into `bytes` of dynamic shared memory.  Static + dynamic
+// shared memory above 48 KB needs the attribute, so it is set for any
+// non-zero request (once per kernel and size: cached).
+bool set_dyn_smem(const void* fn, size_t bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, size_t> done;
+  if (bytes == 0) return true;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = done.find(fn);
+  if (it != done.end() && it->second >= bytes) return true;
+  if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
+      cudaSuccess)
+    return false;
+  done[fn] = bytes;
+  return true;
+}
+
 using K2Fn = void (*)(ih::ScanArgs, ih::RelLut);
 
 ih::Segs segs(const K2Plan& p) { return ih::Segs{p.S, p.nbig, p.S2}; }
@@ -166,9 +184,7 @@ int ctas_per_sm(const K2Plan& p) {
   K2Fn fn = pick_k2(p);
   const size_t smem = k2_ring_smem(p);
   int n = 0;
-  if (fn && (smem <= 48 * 1024 ||
-             cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) ==
-                 cudaSuccess) &&
+  if (fn && set_dyn_smem((const void*)fn, smem) &&
       cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, p.nwarps * 32, smem) == cudaSuccess &&
       n > 0)
     return n;
@@ -442,9 +458,7 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
     dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
     auto kern = al ? ih::k2_colcounts_all<true> : ih::k2_colcounts_all<false>;
     const size_t smem = (size_t)p.nbp * 64 * sizeof(uint32_t);
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-            cudaSuccess)
+    if (!set_dyn_smem((const void*)kern, smem))
       return cuda_fail("k2_colcounts_all smem attribute");
     if (launch(kern, grid, dim3(256), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
                c.fstride, c.lut, segs(p), p.nseg, p.nbp, p.Wp, (uint16_t*)ws, ctot) != cudaSuccess)
@@ -461,9 +475,7 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
                  : (nw == 8 ? ih::k2_colcounts<false, 8>
                             : nw == 4 ? ih::k2_colcounts<false, 4> : ih::k2_colcounts<false, 2>);
   const size_t smem = nw * ih::kCountWarpSmem;
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
+  if (!set_dyn_smem((const void*)kern, smem))
     return cuda_fail("k2_colcounts smem attribute");
   if (launch(kern, grid, dim3(nw * 32), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
              c.fstride, c.lut, segs(p), p.nseg, p.nbp, p.Wp, nslab, (uint16_t*)ws, ctot) != cudaSuccess)
@@ -489,9 +501,7 @@ ih_status launch_k2(const Call& c, const ih::ScanArgs& a, dim3 grid, int threads
   K2Fn fn = pick_k2(c.plan);
   if (!fn) return fail(IH_ERR_PARAM, "internal: no K2 instantiation for plan");
   const size_t smem = k2_ring_smem(c.plan);
-  if (smem > 48 * 1024 &&
-      cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess)
+  if (!set_dyn_smem((const void*)fn, smem))
     return cuda_fail("k2_scan smem attribute");
   // look-back carries read flags a memset just reset: never PDL there
   const bool pdl = c.pdl() && c.plan.carry != ih::CARRY_LOOKBACK;
@@ -696,8 +706,7 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   }
   if (smem <= 160 * 1024 && k4mode == 2) {
     auto k = ih::k4_window_counts_vs;
-    if (smem > 48 * 1024 &&
-        cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    if (!set_dyn_smem((const void*)k, smem))
       return cuda_fail("k4 smem attribute");
     const int64_t cblocks = (C + 4 * threads - 1) / (4 * threads);
     dim3 grid((unsigned)cblocks, (unsigned)(R < 65535 ? R : 65535), (unsigned)nb);

@@ -67,6 +67,10 @@ def test_fuzz_plans_against_oracle(monkeypatch, seed):
         px = np.ascontiguousarray(base[:, offset:])
         view = torch.from_numpy(base).cuda()[:, offset:]
         kernel = "single_pass" if W <= 8192 or "IH_NO_COLTILE" not in env else "auto"
-        got = device.integral_histogram(view, lut, bins, bin_range=(lo, hi), kernel=kernel)
+        try:
+            got = device.integral_histogram(view, lut, bins, bin_range=(lo, hi), kernel=kernel)
+        except Exception as exc:
+            raise AssertionError(f"{exc!r} for {(H, W, bins, lo, hi, env, offset)} "
+                                 f"plan {device.plan(1, H, W, hi - lo)}") from exc
         want = O.compute_crossweave(px, lut, bins)[lo:hi]
         assert np.array_equal(got.cpu().numpy(), want), (H, W, bins, lo, hi, env, offset)
