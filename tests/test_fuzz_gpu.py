@@ -17,7 +17,7 @@ from paper_1711_01919_b200 import device  # noqa: E402
 
 KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY_CLUSTER",
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
-         "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS")
+         "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT")
 
 
 def _case(rng):
@@ -74,3 +74,62 @@ def test_fuzz_plans_against_oracle(monkeypatch, seed):
                                  f"plan {device.plan(1, H, W, hi - lo)}") from exc
         want = O.compute_crossweave(px, lut, bins)[lo:hi]
         assert np.array_equal(got.cpu().numpy(), want), (H, W, bins, lo, hi, env, offset)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_fuzz_frame_batches_and_pitches(monkeypatch, seed):
+    """Frame batches with padded row pitch and frame stride (views into a
+    larger buffer), random plan knobs; every frame equals the oracle."""
+    rng = np.random.default_rng(2000 + seed)
+    for _ in range(10):
+        F = int(rng.integers(1, 6))
+        H = int(rng.choice([1, 5, 40, 333]))
+        W = int(rng.choice([1, 17, 128, 700, 2100, 4097]))
+        bins = int(rng.choice([1, 3, 32, 256]))
+        for k in KNOBS:
+            monkeypatch.delenv(k, raising=False)
+        if rng.random() < 0.6:
+            monkeypatch.setenv("IH_NSEG", str(int(rng.integers(1, 12))))
+        if rng.random() < 0.3:
+            monkeypatch.setenv("IH_TAIL_PCT", "30")
+        pad_w, pad_h = int(rng.choice([0, 16, 5])), int(rng.choice([0, 2]))
+        base = rng.integers(0, 256, (F, H + pad_h, W + pad_w), dtype=np.uint8)
+        view = torch.from_numpy(base).cuda()[:, :H, :W]
+        lut = O.np_uniform_table(bins)
+        got = device.integral_histogram(view, lut, bins).cpu().numpy()
+        for f in range(F):
+            want = O.compute_crossweave(np.ascontiguousarray(base[f, :H, :W]), lut, bins)
+            assert np.array_equal(got[f], want), (F, H, W, bins, pad_w, pad_h, f)
+
+
+@pytest.mark.parametrize("seed", range(3))
+def test_fuzz_queries(monkeypatch, seed):
+    """K3 regions, K4 windows (every kernel variant) and K5 maps (table and
+    direct) on random tensors against the oracle / numpy restatement."""
+    rng = np.random.default_rng(3000 + seed)
+    for _ in range(6):
+        H, W = int(rng.integers(1, 200)), int(rng.integers(1, 1500))
+        bins = int(rng.choice([1, 4, 17, 64]))
+        px = rng.integers(0, 256, (H, W), dtype=np.uint8)
+        full = O.compute_crossweave(px, O.np_uniform_table(bins), bins)
+        t = torch.from_numpy(full.view(np.int32)).cuda().view(torch.uint32)
+        regs = []
+        for _ in range(50):
+            r0, r1 = sorted(rng.integers(0, H, 2).tolist())
+            c0, c1 = sorted(rng.integers(0, W, 2).tolist())
+            regs.append((r0, c0, r1, c1))
+        assert np.array_equal(device.region_histograms(t, regs).cpu().numpy(),
+                              O.region_histograms(full, regs))
+        h, w = int(rng.integers(1, H + 1)), int(rng.integers(1, W + 1))
+        want = O.window_counts(full, h, w)
+        for mode in ("0", "1", "2"):
+            monkeypatch.setenv("IH_K4_MODE", mode)
+            assert np.array_equal(device.window_counts(t, h, w).cpu().numpy(), want), (H, W, h, w, mode)
+        tmpl = rng.random(bins)
+        tmpl /= tmpl.sum()
+        for metric in ("intersection", "bhattacharyya"):
+            ref = O.np_likelihood_map(full, tmpl, h, w, metric)
+            for direct in ("0", "1"):
+                monkeypatch.setenv("IH_K5_DIRECT", direct)
+                got = device.likelihood_map(t, tmpl, h, w, metric).cpu().numpy()
+                assert np.abs(got - ref).max() < 1e-12, (H, W, h, w, metric, direct)
