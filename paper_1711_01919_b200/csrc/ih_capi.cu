@@ -241,7 +241,8 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   // Each segment costs a u16 count slot of 1/(2S) of the output (mostly L2).
   const int64_t slots = (int64_t)kNumSMs * ctas_per_sm(p);
   const int64_t units = frames * p.ngroups * p.T;
-  const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", 32);
+  // 32-row minimum segments; 16 for short images (512^2: 24.0 -> 19.4 us/call)
+  const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", H >= 256 && H <= 768 ? 16 : 32);
   const int64_t max_seg = (H + min_rows - 1) / min_rows;
   const bool many = units * 4 >= slots;  // >= a quarter wave without segments
   double waves = many ? 4.0 : (p.big ? 8.0 : 2.0);

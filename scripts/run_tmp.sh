@@ -1,3 +1,4 @@
 mkdir -p gpurun_out
-(for v in 46 48 28 86 84; do for ry in 37 148 296; do IH_K4_VARIANT=$v IH_K4_ROWS_GRID=$ry timeout 600 python scripts/bench_queries.py 2>&1 | grep "k4_" | head -1 | sed "s/^/v$v ry$ry /"; done; done) > gpurun_out/queries_k4c.jsonl
+(for tc in 16 2 1; do for n in 8 16 32; do IH_TILE_CHUNKS=$tc IH_NSEG=$n IH_MIN_SEG_ROWS=8 timeout 300 python scripts/graph_time.py 512 | sed "s/^/tc$tc n$n /"; done; done
+for tc in 16 4 2; do IH_TILE_CHUNKS=$tc timeout 300 python scripts/graph_time.py hd1 | sed "s/^/tc$tc /"; done) > gpurun_out/small_tc.jsonl 2>&1
 echo done
