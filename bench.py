@@ -285,8 +285,13 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     brange = (b0, b1) if active else None
     tuned = None
     if args.autotune and active:  # measured row-segment count for this shape (warm-up phase)
+        # the whole call (prepare + scan): tuning the scan alone picked many
+        # short segments whose prepass, even overlapped, cost more (HD x8:
+        # step 0.80 vs 0.88; profiles/r01f/autotune_objective.txt)
+        objective = "call"
         tuned = device.autotune(nloc, wl.height, wl.width, wl.bins, bin_range=brange, device=dev,
-                                images=d_img[:nloc], out=out[:nloc])
+                                images=d_img[:nloc], out=out[:nloc], objective=objective)
+        tuned["objective"] = objective
     plan = device.plan(nloc, wl.height, wl.width, nb,
                        aligned16=d_img.data_ptr() % 16 == 0) if active else {"launches": 0}
 

@@ -143,7 +143,7 @@ def segment_candidates(frames: int, height: int, width: int, slab_bins: int) -> 
 
 
 def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, device=None,
-             candidates=None, reps: int = 5, images=None, out=None) -> dict:
+             candidates=None, reps: int = 5, images=None, out=None, objective: str = "call") -> dict:
     """Measure integral_histogram (prepare + scan, CUDA-graph replay) for each
     candidate row-segment count on random frames of this shape, then tail
     splits (10/20/30 % of the rows in quarter-height segments run last) for the
@@ -151,7 +151,11 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
     {"segments", "tail_pct", "tail_div", "ms": {"count[/t<pct>]": ms}}.
     Results are bit-identical for every count; only the speed differs.
     ``images`` / ``out`` (CUDA tensors of the call's shapes) avoid allocating
-    a second input and output."""
+    a second input and output.  ``objective="scan"`` times the scan kernel
+    alone (for pipelines that run the prepass of the next batch concurrently,
+    as bench.py does); the default times the whole call."""
+    if objective not in ("call", "scan"):
+        raise ParameterError(f"unknown objective {objective!r}")
     dev = require_cuda(device)
     lo, hi = (0, bins) if bin_range is None else bin_range
     nb = hi - lo
@@ -184,17 +188,26 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
         torch.cuda.synchronize(dev)
         g = torch.cuda.CUDAGraph()
         with torch.cuda.graph(g, stream=side):
-            integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=w)
-        g.replay()
+            if objective == "scan":  # the workspace still holds this plan's tables
+                scan(imgs, lut, bins, out, bin_range=bin_range, stream=side, workspace=w)
+            else:
+                integral_histogram(imgs, lut, bins, bin_range=bin_range, out=out, workspace=w)
         e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
         torch.cuda.synchronize(dev)
         e0.record()
-        for _ in range(reps):
+        g.replay()
+        e1.record()
+        torch.cuda.synchronize(dev)
+        # ~40 ms of replays per candidate (at least `reps`): small shapes get
+        # more repetitions, so their choice is not decided by timing noise
+        n = max(reps, min(200, int(40.0 / max(e0.elapsed_time(e1), 1e-3))))
+        e0.record()
+        for _ in range(n):
             g.replay()
         e1.record()
         torch.cuda.synchronize(dev)
         del g
-        return e0.elapsed_time(e1) / reps
+        return e0.elapsed_time(e1) / n
 
     with torch.cuda.device(dev):
         for n in candidates:

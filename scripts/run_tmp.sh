@@ -1,4 +1,4 @@
 mkdir -p gpurun_out
-(for tc in 16 2 1; do for n in 8 16 32; do IH_TILE_CHUNKS=$tc IH_NSEG=$n IH_MIN_SEG_ROWS=8 timeout 300 python scripts/graph_time.py 512 | sed "s/^/tc$tc n$n /"; done; done
-for tc in 16 4 2; do IH_TILE_CHUNKS=$tc timeout 300 python scripts/graph_time.py hd1 | sed "s/^/tc$tc /"; done) > gpurun_out/small_tc.jsonl 2>&1
+for fr in 64 16 8; do timeout 900 python bench.py --frames $fr --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_r_hd$fr.json 2>> gpurun_out/bench_r.err; done
+timeout 900 python bench.py --workload 4k128 --e2e-steps 0 --no-cpu-baseline > gpurun_out/bench_r_4k128.json 2>> gpurun_out/bench_r.err
 echo done
