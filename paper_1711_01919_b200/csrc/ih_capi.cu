@@ -100,6 +100,7 @@ struct K2Plan {
   int T = 1;         // column tiles (colt)
   int TW = 0;        // tile width = nwarps * cpl * 128
   bool colt = false; // column-tiled instantiation (W > 2048 unless IH_NO_COLTILE)
+  bool staged = false;  // experimental TMA bulk-store epilogue (IH_STAGED_STORES)
   int slots = 0;     // resident CTAs of the scan kernel (SMs x CTAs per SM)
   int64_t units = 0; // scan CTAs per row segment (frames x bin groups x tiles)
   int carry = 0;     // ih::Carry: NONE (nseg == 1), TABLE or LOOKBACK
@@ -148,8 +149,17 @@ K2Fn pick_carry(int carry, bool colt) {
     default: return ih::k2_scan<CPL, R, VEC, TMA, ih::CARRY_NONE, MAXT, false>;
   }
 }
+template <int R>
+K2Fn pick_staged(int carry) {
+  return carry == ih::CARRY_TABLE ? ih::k2_scan<1, R, true, true, ih::CARRY_TABLE, 512, false, true>
+                                  : ih::k2_scan<1, R, true, true, ih::CARRY_NONE, 512, false, true>;
+}
+
 template <int CPL, int R>
 K2Fn pick_vt(const K2Plan& p) {
+  if constexpr (CPL == 1 && R <= 2) {
+    if (p.staged) return pick_staged<R>(p.carry);
+  }
   if constexpr (CPL == 1) {  // 1024-thread variants: CPL 1, aligned fast path only
     if (p.big) return pick_carry<CPL, R, true, true, 1024>(p.carry, false);
   } else {
@@ -175,7 +185,8 @@ K2Fn pick_k2(const K2Plan& p) {
 size_t k2_ring_smem(const K2Plan& p) {
   if (!p.tma) return 0;
   const int nst = p.R >= 4 ? 2 : (p.R == 2 ? 4 : 8);  // ih::Ring<R>::kStages
-  return (size_t)nst * p.R * p.TW;
+  const size_t stage = p.staged ? (size_t)p.R * ih::kGroup * p.TW * sizeof(uint32_t) : 0;
+  return (size_t)nst * p.R * p.TW + stage;
 }
 
 // Resident CTAs per SM for the plan's kernel (occupancy API); a register-based
@@ -230,6 +241,9 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (r_env == 1 || r_env == 2 || r_env == 4) p.R = (int)r_env;
   const int rmax = p.cpl == 1 ? 4 : p.cpl == 2 ? 2 : 1;
   if (p.R > rmax) p.R = rmax;
+  // experimental staged stores: full-width HD-type kernel, R <= 2 (smem)
+  p.staged = env_int("IH_STAGED_STORES", 0) != 0 && !p.colt && !p.big && p.cpl == 1 && vec && tma;
+  if (p.staged && p.R > 2) p.R = 2;
   p.ngroups = (nb + ih::kGroup - 1) / ih::kGroup;
   p.nbp = p.ngroups * ih::kGroup;
   p.carry = ih::CARRY_TABLE;  // for the occupancy query; fixed up below
@@ -318,6 +332,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   else if (want_cluster && cluster_ok) p.carry = ih::CARRY_CLUSTER;
   else if (p.colt) p.carry = ih::CARRY_TABLE;
   else p.carry = env_int("IH_CARRY_LOOKBACK", 0) ? ih::CARRY_LOOKBACK : ih::CARRY_TABLE;
+  if (p.carry == ih::CARRY_LOOKBACK || p.carry == ih::CARRY_CLUSTER) p.staged = false;
   return p;
 }
 

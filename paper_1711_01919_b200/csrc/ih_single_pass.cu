@@ -463,9 +463,13 @@ __device__ __forceinline__ uint32_t warp_scan_pred(uint32_t x) {
 // MAXT: launch bound -- 512 (<= 16 warps, up to 128 registers) or 1024
 // (<= 32 warps at <= 64 registers: full SM occupancy from one CTA).
 // COLT kernels must keep two 16-warp CTAs per SM (<= 64 registers).
-template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT, bool COLT>
+// STG (experimental, IH_STAGED_STORES=1): output rows are staged in shared
+// memory ([R][4 bins][TW] u32 after the input ring) and written by TMA bulk
+// copies of whole plane rows (one per bin and row) instead of per-lane stores.
+template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT, bool COLT, bool STG = false>
 __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut lut) {
   constexpr int NST = Ring<R>::kStages;
+  static_assert(!STG || (TMA && VEC && !COLT && CPL == 1), "staged stores: TMA, VEC, CPL 1");
   static_assert(!(COLT && CARRY == CARRY_LOOKBACK), "column tiles use table carries");
   static_assert(!(COLT && CARRY == CARRY_CLUSTER), "column tiles use table carries");
   constexpr bool CL = CARRY == CARRY_CLUSTER;
@@ -869,6 +873,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
 #pragma unroll
   for (int k = 0; k < CPL; ++k) prow[k] = plane0 + rs * W + ct + cl[k];
   const bool full_group = nbins_here == kGroup;
+  uint32_t* stage = STG ? reinterpret_cast<uint32_t*>(ring + (size_t)NST * R * a.TW) : nullptr;
   for (int b = nb_count; b < nb_total; ++b) {
     const int bi = b - nb_count;
     const int buf = bi & 1;
@@ -910,6 +915,8 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
       lnext = rn < re ? __ldg(reinterpret_cast<const uint4*>(lrow + rn * a.nbp))
                       : make_uint4(0u, 0u, 0u, 0u);
     }
+    if (STG && threadIdx.x == 0)  // last batch's bulk stores have read the stage buffer
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     __syncthreads();  // totals visible; every warp is done reading the ring stage
     if (TMA && threadIdx.x == 0 && b + NST < nb_total) issue(b + NST);
 #pragma unroll
@@ -933,7 +940,13 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
             for (int i = 0; i < kGroup; ++i) acc[k][j][i] += run[i] + byte_of(v[rr][k][j], i);
 #pragma unroll
           for (int i = 0; i < kGroup; ++i) run[i] += byte_of(ct[rr][k], i);
-          if (colok[k]) {
+          if (STG) {
+            uint32_t* sp = stage + (size_t)rr * kGroup * a.TW + cl[k];
+#pragma unroll
+            for (int i = 0; i < kGroup; ++i)
+              *reinterpret_cast<uint4*>(sp + (size_t)i * a.TW) =
+                  make_uint4(acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
+          } else if (colok[k]) {
             uint32_t* p = prow[k];
             if (VEC && full_group) {
 #pragma unroll
@@ -958,7 +971,23 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
         }
       }
     }
+    if (STG) {  // the batch's rows are staged: bulk-copy whole plane rows out
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        for (int rr = 0; rr < rows; ++rr)
+          for (int i = 0; i < nbins_here; ++i) {
+            uint32_t* dst = plane0 + (int64_t)i * plane_elems + (r0 + rr) * W;
+            asm volatile(
+                "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
+                "r"(smem_u32(stage + ((size_t)rr * kGroup + i) * a.TW)), "r"((uint32_t)(W * 4))
+                : "memory");
+          }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+    }
   }
+  if (STG && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (CL) cluster_wait_acquire();  // no CTA leaves while a neighbour may read its ccnt[]
   if (a.trace) {  // debug timeline (uniform branch)
     __syncthreads();

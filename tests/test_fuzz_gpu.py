@@ -17,7 +17,8 @@ from paper_1711_01919_b200 import device  # noqa: E402
 
 KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY_CLUSTER",
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
-         "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT")
+         "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT",
+         "IH_STAGED_STORES")
 
 
 def _case(rng):
@@ -41,7 +42,7 @@ def _case(rng):
         env["IH_TABLE_SUM_MAX"] = "1"
     env["IH_ROWS_PER_BATCH"] = str(int(rng.choice([1, 2, 4])))
     for k, p in (("IH_NO_TMA", 0.2), ("IH_NO_COLTILE", 0.2), ("IH_COLCOUNTS_SLAB", 0.2),
-                 ("IH_NO_PDL", 0.2)):
+                 ("IH_NO_PDL", 0.2), ("IH_STAGED_STORES", 0.25)):
         if rng.random() < p:
             env[k] = "1"
     if rng.random() < 0.2:
