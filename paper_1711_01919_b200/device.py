@@ -216,7 +216,10 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
         n0 = min(times, key=times.get)[0]
         if n0 > 1:
             for tail_pct in (10, 20, 30):
-                times[(n0, tail_pct, 4)] = measure(n0, tail_pct, 4)
+                set_plan_hint(frames, height, width, nb, n0, tail_pct, 4)
+                p = plan(frames, height, width, nb)
+                if p["big_segments"] < p["segments"]:  # the split applies to this shape
+                    times[(n0, tail_pct, 4)] = measure(n0, tail_pct, 4)
     best = min(times, key=times.get)
     set_plan_hint(frames, height, width, nb, *best)
     return {"segments": best[0], "tail_pct": best[1], "tail_div": best[2],
