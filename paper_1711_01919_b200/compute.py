@@ -177,6 +177,6 @@ def compute_frames(frames, spec: BinSpec, bin_range=None, kernel: str = "auto", 
     if isinstance(frames, np.ndarray):
         frames = torch.from_numpy(np.ascontiguousarray(frames, dtype=np.uint8))
     if not frames.is_cuda:
-        frames = frames.to(device.require_cuda())
+        frames = device.upload_frames(frames)
     return device.integral_histogram(frames, spec.table, spec.bins, bin_range=bin_range,
                                      kernel=kernel)

@@ -66,14 +66,17 @@ __device__ __forceinline__ void griddep_launch_dependents() {
 
 // Streaming (evict-first) 16-byte / 4-byte global stores: every output byte
 // is written exactly once and never re-read by the producing kernel.
+#ifndef IH_STORE_HINT
+#define IH_STORE_HINT ".cs"
+#endif
 __device__ __forceinline__ void st_stream_v4(uint32_t* p, uint32_t a, uint32_t b, uint32_t c,
                                              uint32_t d) {
-  asm volatile("st.global.cs.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c),
-               "r"(d)
+  asm volatile("st.global" IH_STORE_HINT ".v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b),
+               "r"(c), "r"(d)
                : "memory");
 }
 __device__ __forceinline__ void st_stream(uint32_t* p, uint32_t a) {
-  asm volatile("st.global.cs.u32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
+  asm volatile("st.global" IH_STORE_HINT ".u32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
 }
 
 // Build the packed one-hot table of one bin group in shared memory:

@@ -28,6 +28,10 @@ WL = {
   "8k256/2": (8192, 8192, 256, 1, (0, 128)),
   "8k256/4": (8192, 8192, 256, 1, (0, 64)),
   "512x8": (512, 512, 32, 8, None),
+  "hd8w1921": (1921, 1080, 32, 8, None),
+  "hd8w1922": (1922, 1080, 32, 8, None),
+  "hd8w1924": (1924, 1080, 32, 8, None),
+  "hd64w1921": (1921, 1080, 32, 64, None),
 }
 def run(name, reps=5, kernel="auto"):
     W, H, B, F, br = WL[name]

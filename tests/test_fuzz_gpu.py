@@ -18,7 +18,7 @@ from paper_1711_01919_b200 import device  # noqa: E402
 KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY_CLUSTER",
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
          "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT",
-         "IH_STAGED_STORES")
+         "IH_STAGED_STORES", "IH_NO_RESTAGE")
 
 
 def _case(rng):
@@ -50,6 +50,8 @@ def _case(rng):
     if rng.random() < 0.2:
         env["IH_MIN_SEG_ROWS"] = "4"
     offset = int(rng.choice([0, 0, 1, 3]))
+    if rng.random() < 0.5:  # unaligned rows: the kernels' own LDG path
+        env["IH_NO_RESTAGE"] = "1"
     return H, W, bins, lo, hi, env, offset
 
 

@@ -26,7 +26,7 @@ def crc_of(t) -> str:
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
     for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
-              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_CLUSTER"):
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_CLUSTER", "IH_NO_RESTAGE"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -147,8 +147,13 @@ def test_tall_image_sum_mode(rng):
     assert np.array_equal(got, O.compute_crossweave(px, lut, 3))
 
 
-def test_unaligned_rows_and_odd_widths(rng):
-    """ALIGNED=false (odd pitch / offset) and VEC=false (W % 4 != 0) paths."""
+@pytest.mark.parametrize("restage", [True, False])
+def test_unaligned_rows_and_odd_widths(monkeypatch, rng, restage):
+    """ALIGNED=false (odd pitch / offset) and VEC=false (W % 4 != 0) paths:
+    through the device API's 16-byte restaging (TMA path) and, with
+    IH_NO_RESTAGE=1, the kernels' own unaligned (LDG) path."""
+    if not restage:
+        monkeypatch.setenv("IH_NO_RESTAGE", "1")
     for (h, w, bins) in [(37, 101, 16), (64, 255, 7), (19, 1025, 64), (5, 3, 2)]:
         base = rng.integers(0, 256, (h, w + 7), dtype=np.uint8)
         px = np.ascontiguousarray(base[:, 3:3 + w])
