@@ -32,6 +32,13 @@ WL = {
   "hd8w1922": (1922, 1080, 32, 8, None),
   "hd8w1924": (1924, 1080, 32, 8, None),
   "hd64w1921": (1921, 1080, 32, 64, None),
+  "hd64b1": (1920, 1080, 1, 64, None),
+  "hd64b2": (1920, 1080, 2, 64, None),
+  "hd64b4": (1920, 1080, 4, 64, None),
+  "hd64b8": (1920, 1080, 8, 64, None),
+  "hd64b16": (1920, 1080, 16, 64, None),
+  "hd64b37": (1920, 1080, 37, 64, None),
+  "hd64b64": (1920, 1080, 64, 64, None),
 }
 def run(name, reps=5, kernel="auto"):
     W, H, B, F, br = WL[name]
