@@ -75,6 +75,10 @@ __device__ __forceinline__ void st_stream_v4(uint32_t* p, uint32_t a, uint32_t b
                "r"(c), "r"(d)
                : "memory");
 }
+__device__ __forceinline__ void st_stream_v2(uint32_t* p, uint32_t a, uint32_t b) {
+  asm volatile("st.global" IH_STORE_HINT ".v2.u32 [%0], {%1, %2};" ::"l"(p), "r"(a), "r"(b)
+               : "memory");
+}
 __device__ __forceinline__ void st_stream(uint32_t* p, uint32_t a) {
   asm volatile("st.global" IH_STORE_HINT ".u32 [%0], %1;" ::"l"(p), "r"(a) : "memory");
 }

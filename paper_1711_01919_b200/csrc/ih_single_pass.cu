@@ -959,9 +959,24 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
                   if (VEC) {
                     st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
                   } else {
+                    // W % 4 != 0: rows start at varying 4-byte offsets; use the
+                    // widest store this row's alignment allows (warp-uniform:
+                    // lanes are 16 bytes apart)
+                    const uint32_t al = (uint32_t)reinterpret_cast<uintptr_t>(p) & 15u;
+                    if (al == 0u && !inval[k][3]) {
+                      st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
+                    } else if ((al & 7u) == 0u && !inval[k][3]) {
+                      st_stream_v2(p, acc[k][0][i], acc[k][1][i]);
+                      st_stream_v2(p + 2, acc[k][2][i], acc[k][3][i]);
+                    } else if (!inval[k][3]) {  // odd word offset: 4 + 8 + 4 bytes
+                      st_stream(p, acc[k][0][i]);
+                      st_stream_v2(p + 1, acc[k][1][i], acc[k][2][i]);
+                      st_stream(p + 3, acc[k][3][i]);
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
-                      if (!inval[k][j]) st_stream(p + j, acc[k][j][i]);
+                      for (int j = 0; j < 4; ++j)
+                        if (!inval[k][j]) st_stream(p + j, acc[k][j][i]);
+                    }
                   }
                 }
               }
