@@ -39,6 +39,14 @@ WL = {
   "hd64b16": (1920, 1080, 16, 64, None),
   "hd64b37": (1920, 1080, 37, 64, None),
   "hd64b64": (1920, 1080, 64, 64, None),
+  "vga64": (640, 480, 32, 64, None),
+  "svga64": (800, 600, 32, 64, None),
+  "xga64": (1024, 768, 32, 64, None),
+  "hd720x64": (1280, 720, 32, 64, None),
+  "wxga64": (1366, 768, 32, 64, None),
+  "hdp64": (1600, 900, 32, 64, None),
+  "qhd16": (2560, 1440, 32, 16, None),
+  "uhd8": (3840, 2160, 32, 8, None),
 }
 def run(name, reps=5, kernel="auto"):
     W, H, B, F, br = WL[name]
