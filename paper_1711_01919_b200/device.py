@@ -249,6 +249,53 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
             "ms": {f"{k[0]}" + (f"/t{k[1]}" if k[1] else ""): round(v, 4) for k, v in times.items()}}
 
 
+class GraphedIntegralHistogram:
+    """Repeated integral histograms of one shape as a captured CUDA graph.
+
+    For serving loops over small frames, where the per-call host work
+    (argument checks, planning, launches) is comparable to the kernels: the
+    call (prepare + scan) is captured once on static buffers and each
+    ``__call__`` is one H2D/D2D copy into the static input plus one graph
+    replay.  Returns the static (F, B_slab, H, W) output tensor (overwritten
+    by the next call; ``.clone()`` to keep it).  Bit-identical to
+    integral_histogram.
+    """
+
+    def __init__(self, frames: int, height: int, width: int, table, bins: int, bin_range=None,
+                 device=None, kernel: str = "auto"):
+        self.dev = require_cuda(device)
+        lo, hi = (0, bins) if bin_range is None else bin_range
+        pitch = (width + 15) // 16 * 16  # TMA-aligned rows
+        self._buf = torch.zeros((frames, height, pitch), dtype=torch.uint8, device=self.dev)
+        self.images = self._buf[:, :, :width]
+        self.out = empty_output(frames, hi - lo, height, width, self.dev)
+        self._ws = torch.empty(max(workspace_bytes(frames, height, width, hi - lo, kernel), 16),
+                               dtype=torch.uint8, device=self.dev)
+        self._args = (table, bins, bin_range, kernel)
+        self.stream = torch.cuda.Stream(self.dev)
+        with torch.cuda.device(self.dev):
+            integral_histogram(self.images, table, bins, bin_range=bin_range, out=self.out,
+                               kernel=kernel, workspace=self._ws)  # warm: attributes
+            torch.cuda.synchronize(self.dev)
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph, stream=self.stream):
+                integral_histogram(self.images, table, bins, bin_range=bin_range, out=self.out,
+                                   kernel=kernel, workspace=self._ws)
+
+    def __call__(self, images=None) -> torch.Tensor:
+        """``images``: (F, H, W) / (H, W) uint8, host (pinned for async) or
+        CUDA; None replays on the current contents of ``self.images``."""
+        cur = torch.cuda.current_stream(self.dev)
+        if images is not None:
+            src = images if isinstance(images, torch.Tensor) else torch.from_numpy(
+                np.ascontiguousarray(images, dtype=np.uint8))
+            self.images.copy_(src.view(self.images.shape), non_blocking=True)
+        self.stream.wait_stream(cur)
+        self.graph.replay()
+        cur.wait_stream(self.stream)
+        return self.out
+
+
 def empty_output(frames: int, slab_bins: int, height: int, width: int, device) -> torch.Tensor:
     return torch.empty((frames, slab_bins, height, width), dtype=torch.uint32, device=device)
 

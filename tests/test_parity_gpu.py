@@ -616,3 +616,18 @@ def test_devices_kwarg_single_process(rng, shard, out):
                           want[0])
     t = ih.compute_frames(frames, ih.BinSpec.uniform(11), devices=[0, 0], shard=shard)
     assert np.array_equal(t.cpu().numpy(), want)
+
+
+def test_graphed_integral_histogram(rng):
+    """GraphedIntegralHistogram: capture once, replay with new frames (host or
+    device, unaligned width), bit-identical to the oracle each time."""
+    for (F, H, W, bins, br) in [(2, 90, 301, 13, None), (1, 1080, 1920, 32, (8, 24))]:
+        g = device.GraphedIntegralHistogram(F, H, W, O.np_uniform_table(bins), bins, bin_range=br)
+        lo, hi = br or (0, bins)
+        for rep in range(3):
+            frames = rng.integers(0, 256, (F, H, W), dtype=np.uint8)
+            src = frames if rep % 2 == 0 else torch.from_numpy(frames).cuda()
+            out = g(src).cpu().numpy()
+            for f in range(F):
+                want = O.compute_crossweave(frames[f], O.np_uniform_table(bins), bins)[lo:hi]
+                assert np.array_equal(out[f], want), (F, H, W, rep, f)
