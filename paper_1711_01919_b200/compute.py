@@ -64,6 +64,7 @@ SCAN_TRANSPOSE_SCAN = Strategy("sts")
 
 
 def wavefront(tile: int = DEFAULT_TILE) -> Strategy:
+    """Strategy("wavefront", tile) (reference strategies.py:58-59)."""
     return Strategy("wavefront", tile)
 
 

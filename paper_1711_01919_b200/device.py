@@ -25,6 +25,7 @@ _workspaces: dict[int, torch.Tensor] = {}
 
 
 def require_cuda(device=None) -> torch.device:
+    """The CUDA device to run on; raises DeviceError when none exists (no CPU fallback)."""
     if not torch.cuda.is_available():
         raise DeviceError("no CUDA device visible: the B200 engine has no CPU fallback")
     _native.lib()
@@ -119,6 +120,7 @@ def _prepare_args(images, table, bins, bin_range, kernel, stream) -> _Args:
 
 
 def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto") -> int:
+    """Device scratch bytes integral_histogram needs for this shape (ih_workspace_bytes)."""
     return int(_native.lib().ih_workspace_bytes(frames, height, width, slab_bins,
                                                 _native.KERNELS[kernel]))
 
@@ -297,6 +299,7 @@ class GraphedIntegralHistogram:
 
 
 def empty_output(frames: int, slab_bins: int, height: int, width: int, device) -> torch.Tensor:
+    """An uninitialised (F, B_slab, H, W) uint32 output tensor on `device`."""
     return torch.empty((frames, slab_bins, height, width), dtype=torch.uint32, device=device)
 
 

@@ -76,6 +76,7 @@ def read_pgm(data: bytes) -> GrayImage:
 
 
 def write_pgm(img: GrayImage) -> bytes:
+    """Binary PGM (P5) bytes of an image (reference imgio.py:75-77)."""
     return b"P5\n%d %d\n255\n" % (img.width, img.height) + img.pixels.tobytes()
 
 
@@ -92,6 +93,7 @@ def write_map_pgm(values) -> bytes:
 
 # ---------------------------------------------------------------------- IHST
 def ihst_header(bins: int, width: int, height: int) -> bytes:
+    """The 16-byte IHST header `<4sHHII` (reference imgio.py:28)."""
     return _HDR.pack(IHST_MAGIC, IHST_VERSION, bins, width, height)
 
 
@@ -102,6 +104,7 @@ def serialize_ih(ih: IntegralHistogram) -> bytes:
 
 
 def deserialize_ih(data: bytes) -> IntegralHistogram:
+    """IHST bytes -> IntegralHistogram, with the reference's format checks (imgio.py:97-117)."""
     if len(data) < IHST_HEADER_BYTES:
         raise FormatError("tensor file shorter than its header")
     magic, version, bins, width, height = _HDR.unpack_from(data)
@@ -133,6 +136,7 @@ class TensorFileSink:
         return IHST_HEADER_BYTES + 4 * (b * self.height + row) * self.width
 
     def write(self, bin_start, bin_stop, row_start, row_stop, data):
+        """TensorSink.write: place a (bins, rows, W) chunk at its final file offset (reference imgio.py:134-139)."""
         blocks = np.asarray(data)
         with self._lock:
             for k, b in enumerate(range(bin_start, bin_stop)):
@@ -140,6 +144,7 @@ class TensorFileSink:
                 os.pwrite(self._fd, rows.tobytes(), self._offset(b, row_start))
 
     def close(self):
+        """Close the file (reference imgio.py:141-142)."""
         if self._fd is not None:
             os.close(self._fd)
             self._fd = None
