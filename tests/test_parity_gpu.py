@@ -631,3 +631,22 @@ def test_graphed_integral_histogram(rng):
             for f in range(F):
                 want = O.compute_crossweave(frames[f], O.np_uniform_table(bins), bins)[lo:hi]
                 assert np.array_equal(out[f], want), (F, H, W, rep, f)
+
+
+@pytest.mark.parametrize("shard", ["bins", "frames"])
+def test_c7_device_count_determinism(rng, shard):
+    """acceptance C7 extended to device counts 1/2/4/8 -- the
+    assembled tensor is byte-identical for every count (the one GPU stands in
+    for each device, on separate streams)."""
+    from paper_1711_01919_b200 import multi
+
+    frames = rng.integers(0, 256, (8, 70, 517), dtype=np.uint8)
+    lut = O.np_uniform_table(37)
+    ref = None
+    for g in (1, 2, 4, 8):
+        got = multi.integral_histogram_devices(frames, lut, 37, [0] * g, shard=shard, out="host")
+        if ref is None:
+            ref = got
+            for f in range(8):
+                assert np.array_equal(got[f], O.compute_crossweave(frames[f], lut, 37))
+        assert np.array_equal(got, ref), g
