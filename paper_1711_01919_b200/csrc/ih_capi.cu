@@ -101,6 +101,7 @@ struct K2Plan {
   int TW = 0;        // tile width = nwarps * cpl * 128
   bool colt = false; // column-tiled instantiation (W > 2048 unless IH_NO_COLTILE)
   bool staged = false;  // experimental TMA bulk-store epilogue (IH_STAGED_STORES)
+  int kb = 4;           // bins per group: 4, or 1/2 with 4/2 rows packed per word (B <= 2)
   int slots = 0;     // resident CTAs of the scan kernel (SMs x CTAs per SM)
   int64_t units = 0; // scan CTAs per row segment (frames x bin groups x tiles)
   int carry = 0;     // ih::Carry: NONE (nseg == 1), TABLE or LOOKBACK
@@ -155,10 +156,28 @@ K2Fn pick_staged(int carry) {
                                   : ih::k2_scan<1, R, true, true, ih::CARRY_NONE, 512, false, true>;
 }
 
+template <int KB, bool VEC, bool TMA>
+K2Fn pick_rowpack_c(int carry) {
+  return carry == ih::CARRY_TABLE
+             ? ih::k2_scan<1, 4, VEC, TMA, ih::CARRY_TABLE, 512, false, false, KB>
+             : ih::k2_scan<1, 4, VEC, TMA, ih::CARRY_NONE, 512, false, false, KB>;
+}
+template <int KB>
+K2Fn pick_rowpack(const K2Plan& p) {
+  if (p.vec && p.tma) return pick_rowpack_c<KB, true, true>(p.carry);
+  if (p.vec) return pick_rowpack_c<KB, true, false>(p.carry);
+  if (p.tma) return pick_rowpack_c<KB, false, true>(p.carry);
+  return pick_rowpack_c<KB, false, false>(p.carry);
+}
+
 template <int CPL, int R>
 K2Fn pick_vt(const K2Plan& p) {
   if constexpr (CPL == 1 && R <= 2) {
     if (p.staged) return pick_staged<R>(p.carry);
+  }
+  if constexpr (CPL == 1 && R == 4) {
+    if (p.kb == 1) return pick_rowpack<1>(p);
+    if (p.kb == 2) return pick_rowpack<2>(p);
   }
   if constexpr (CPL == 1) {  // 1024-thread variants: CPL 1, aligned fast path only
     if (p.big) return pick_carry<CPL, R, true, true, 1024>(p.carry, false);
@@ -244,8 +263,17 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   // experimental staged stores: full-width HD-type kernel, R <= 2 (smem)
   p.staged = env_int("IH_STAGED_STORES", 0) != 0 && !p.colt && !p.big && p.cpl == 1 && vec && tma;
   if (p.staged && p.R > 2) p.R = 2;
-  p.ngroups = (nb + ih::kGroup - 1) / ih::kGroup;
-  p.nbp = p.ngroups * ih::kGroup;
+  {  // row packing for 1- and 2-bin slabs (plain / table carries, no column tiles)
+    int32_t tp = 0, td = 0, fl = 0;
+    hint_lookup(frames, H, W, nb, &tp, &td, &fl);
+    const bool rowpack_ok = !p.colt && !p.big && p.cpl == 1 && !p.staged &&
+                            env_int("IH_NO_ROWPACK", 0) == 0 && env_int("IH_CARRY_LOOKBACK", 0) == 0 &&
+                            env_int("IH_CARRY_CLUSTER", 0) == 0 && !(fl & kHintCluster);
+    p.kb = rowpack_ok && nb <= 2 ? nb : ih::kGroup;
+    if (p.kb < ih::kGroup) p.R = 4;
+  }
+  p.ngroups = (nb + p.kb - 1) / p.kb;
+  p.nbp = p.ngroups * p.kb;
   p.carry = ih::CARRY_TABLE;  // for the occupancy query; fixed up below
   // Row segments (measured, scripts/sweep2.py -> profiles/r01_sweep_*.jsonl):
   // every CTA does the same work, so the CTA count should be a whole number
@@ -326,7 +354,8 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   // cluster carries: the segments of a strip are one thread-block cluster
   // (<= 16 CTAs) exchanging counts through distributed shared memory -- one
   // launch, no prepass; CPL-1 512-thread kernels without column tiles, H < 65536
-  const bool cluster_ok = !p.colt && !p.big && p.cpl == 1 && p.nseg <= 16 && H <= 65535;
+  const bool cluster_ok =
+      !p.colt && !p.big && p.cpl == 1 && p.kb == ih::kGroup && p.nseg <= 16 && H <= 65535;
   const bool want_cluster = env_int("IH_CARRY_CLUSTER", (hinted_flags & kHintCluster) ? 1 : 0) != 0;
   if (p.nseg <= 1) p.carry = ih::CARRY_NONE;
   else if (want_cluster && cluster_ok) p.carry = ih::CARRY_CLUSTER;

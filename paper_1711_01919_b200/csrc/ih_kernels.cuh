@@ -99,6 +99,20 @@ __device__ __forceinline__ void build_onehot(uint32_t* oh, const RelLut& lut, in
   }
 }
 
+// The same for a group of KB (1, 2 or 4) bins: byte d of the word counts bin
+// g*KB + d (the row-packed K2 variants put further rows in the higher bytes).
+template <int KB>
+__device__ __forceinline__ void build_onehot_kb(uint32_t* oh, const RelLut& lut, int g) {
+  for (int v = threadIdx.x; v < kOneHotEntries; v += blockDim.x) {
+    uint32_t word = 0;
+    if (v < 256) {
+      uint32_t d = (uint32_t)lut.rel[v] - (uint32_t)(g * KB);
+      if (d < (uint32_t)KB) word = 1u << (8u * d);
+    }
+    oh[v] = word;
+  }
+}
+
 // Load the 4 pixels of one lane in one chunk row and return their 4 one-hot
 // words through the table.  `inval` has bit 8 set for pixel slots at or
 // beyond the right image edge (they map to oh[256 + byte] == 0).

@@ -466,9 +466,20 @@ __device__ __forceinline__ uint32_t warp_scan_pred(uint32_t x) {
 // STG (experimental, IH_STAGED_STORES=1): output rows are staged in shared
 // memory ([R][4 bins][TW] u32 after the input ring) and written by TMA bulk
 // copies of whole plane rows (one per bin and row) instead of per-lane stores.
-template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT, bool COLT, bool STG = false>
+//
+// KB (bins per group, 4/2/1): for B <= 2 the byte lanes of a word carry KR = 4/KB
+// ROWS of KB bins instead of one row of 4 bins, so a warp scan serves KR rows
+// and no lane is wasted on empty bins.
+template <int CPL, int R, bool VEC, bool TMA, int CARRY, int MAXT, bool COLT, bool STG = false,
+          int KB = kGroup>
 __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut lut) {
   constexpr int NST = Ring<R>::kStages;
+  constexpr int KR = kGroup / KB;  // rows packed per word
+  constexpr int NP = R / KR;       // packed passes per batch
+  static_assert(KB == 4 || KB == 2 || KB == 1, "bins per group");
+  static_assert(R % KR == 0, "a batch holds whole packed passes");
+  static_assert(KB == 4 || (!COLT && !STG && CARRY != CARRY_LOOKBACK && CARRY != CARRY_CLUSTER),
+                "row packing: plain or table carries, no column tiles");
   static_assert(!STG || (TMA && VEC && !COLT && CPL == 1), "staged stores: TMA, VEC, CPL 1");
   static_assert(!(COLT && CARRY == CARRY_LOOKBACK), "column tiles use table carries");
   static_assert(!(COLT && CARRY == CARRY_CLUSTER), "column tiles use table carries");
@@ -544,7 +555,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     for (int b = 0; b < NST && b < nb_total; ++b) issue(b);
   }
-  build_onehot(oh, lut, g);
+  build_onehot_kb<KB>(oh, lut, g);
 
   // lane columns: ct + cl[k] + j, j = 0..3 (cl = column inside the tile)
   int cl[CPL];
@@ -565,29 +576,29 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   bool colok[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) colok[k] = ct + cl[k] < W;
-  uint32_t* plane0 = a.out + (f * a.nb + (int64_t)g * kGroup) * plane_elems;
-  const int nbins_here = min(kGroup, a.nb - g * kGroup);
+  uint32_t* plane0 = a.out + (f * a.nb + (int64_t)g * KB) * plane_elems;
+  const int nbins_here = min(KB, a.nb - g * KB);
 
-  uint32_t acc[CPL][4][kGroup];
+  uint32_t acc[CPL][4][KB];
 #pragma unroll
   for (int k = 0; k < CPL; ++k)
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int i = 0; i < kGroup; ++i) acc[k][j][i] = 0u;
+      for (int i = 0; i < KB; ++i) acc[k][j][i] = 0u;
 
   // table carries: sum the count slots above this segment (independent global
   // loads, issued before the first barrier so they overlap the table build)
   if (CARRY == CARRY_TABLE && s > 0) {
     const int64_t plane_sz = (int64_t)a.nbp * a.Wp;
-    const uint16_t* cp = a.colpre + (f * a.nseg) * plane_sz + (int64_t)g * kGroup * a.Wp;
+    const uint16_t* cp = a.colpre + (f * a.nseg) * plane_sz + (int64_t)g * KB * a.Wp;
     if constexpr (COLT) if (t > 0) {
       // the carry also counts the pixels above the segment and left of the
       // tile: the count kernel's per-chunk totals, segments s' < s, chunks
       // left of the tile (spread over the CTA, reduced through sls[])
       const int nch = (int)(a.Wp / kChunk), left = (int)(ct / kChunk);
       uint4 part = make_uint4(0u, 0u, 0u, 0u);
-      const uint32_t* tt = a.chunktot + (f * a.nseg) * nch * a.nbp + g * kGroup;
+      const uint32_t* tt = a.chunktot + (f * a.nseg) * nch * a.nbp + g * KB;
       for (int e = threadIdx.x; e < s * left; e += blockDim.x) {
         const int sp = e / left, x = e - sp * left;
         const uint4 v = __ldg(reinterpret_cast<const uint4*>(tt + ((int64_t)sp * nch + x) * a.nbp));
@@ -608,13 +619,13 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     const int sp0 = a.table_is_prefix ? s : 0;
     const int sp1 = a.table_is_prefix ? s + 1 : s;
     for (int sp = sp0; sp < sp1; sp += U) {
-      uint2 v[U][CPL][kGroup];
+      uint2 v[U][CPL][KB];
 #pragma unroll
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
 #pragma unroll
-          for (int i = 0; i < kGroup; ++i)
+          for (int i = 0; i < KB; ++i)
             v[u][k][i] = sp + u < sp1 ? *reinterpret_cast<const uint2*>(
                                             cp + (sp + u) * plane_sz + i * a.Wp + ct + cl[k])
                                       : make_uint2(0u, 0u);
@@ -623,7 +634,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
 #pragma unroll
-          for (int i = 0; i < kGroup; ++i) {
+          for (int i = 0; i < KB; ++i) {
             acc[k][0][i] += v[u][k][i].x & 0xffffu;
             acc[k][1][i] += v[u][k][i].x >> 16;
             acc[k][2][i] += v[u][k][i].y & 0xffffu;
@@ -638,7 +649,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   const uint32_t* lrow = nullptr;
   uint4 lnext = make_uint4(0u, 0u, 0u, 0u);
   if (COLT && t > 0) {
-    lrow = a.rowleft + ((f * (a.T - 1) + (t - 1)) * H) * a.nbp + g * kGroup;
+    lrow = a.rowleft + ((f * (a.T - 1) + (t - 1)) * H) * a.nbp + g * KB;
     if (warp == 0 && lane < R && rs + lane < re)
       lnext = __ldg(reinterpret_cast<const uint4*>(lrow + (rs + lane) * a.nbp));
   }
@@ -659,7 +670,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     }
   };
 
-  if (CL) {
+  if constexpr (CL) {
     // ---- pass 0 (all but the last segment): per-column counts of this
     // segment's rows, 4 bins in two words of 16-bit lanes, into ccnt[]
     if (count_pass) {
@@ -717,8 +728,8 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     cluster_arrive_release();  // done reading the others' ccnt (waited at exit)
   }
 
-  if (CARRY == CARRY_LOOKBACK) {
-    const int64_t ntile_vec = (int64_t)kGroup * a.Wp;  // u32 per published vector
+  if constexpr (CARRY == CARRY_LOOKBACK) {
+    const int64_t ntile_vec = (int64_t)KB * a.Wp;  // u32 per published vector
     const uint32_t tile = s_tile;
     uint32_t* flags = a.lb_flags;
     uint32_t* agg = a.lb_agg;
@@ -756,7 +767,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
       uint32_t* dst = agg + (int64_t)tile * ntile_vec;
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
-        uint32_t cnt[kGroup][4];
+        uint32_t cnt[KB][4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           cnt[0][j] = ce[k][j] & 0xffffu;
@@ -765,12 +776,12 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
           cnt[3][j] = co[k][j] >> 16;
         }
 #pragma unroll
-        for (int i = 0; i < kGroup; ++i)
+        for (int i = 0; i < KB; ++i)
           __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + cl[k]),
                  make_uint4(cnt[i][0], cnt[i][1], cnt[i][2], cnt[i][3]));
         if (s == 0) {  // segment 0: its aggregate is its inclusive prefix
 #pragma unroll
-          for (int i = 0; i < kGroup; ++i)
+          for (int i = 0; i < KB; ++i)
             __stcg(reinterpret_cast<uint4*>(incl + (int64_t)tile * ntile_vec + i * a.Wp + cl[k]),
                    make_uint4(cnt[i][0], cnt[i][1], cnt[i][2], cnt[i][3]));
         }
@@ -794,7 +805,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
 #pragma unroll
-          for (int i = 0; i < kGroup; ++i) {
+          for (int i = 0; i < KB; ++i) {
             const uint4 x = __ldcg(reinterpret_cast<const uint4*>(src + i * a.Wp + cl[k]));
             acc[k][0][i] += x.x;
             acc[k][1][i] += x.y;
@@ -810,7 +821,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
 #pragma unroll
         for (int k = 0; k < CPL; ++k)
 #pragma unroll
-          for (int i = 0; i < kGroup; ++i) {
+          for (int i = 0; i < KB; ++i) {
             const uint4 x = __ldcg(reinterpret_cast<const uint4*>(own + i * a.Wp + cl[k]));
             __stcg(reinterpret_cast<uint4*>(dst + i * a.Wp + cl[k]),
                    make_uint4(acc[k][0][i] + x.x, acc[k][1][i] + x.y, acc[k][2][i] + x.z,
@@ -825,19 +836,19 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
 
   // ---- segment carry: acc(c) <- sum_{c' <= c} acc(c') = H_b(r_s - 1, c)
   if (CARRY != CARRY_NONE && s > 0) {
-    uint32_t run[kGroup] = {0u, 0u, 0u, 0u};
+    uint32_t run[KB] = {};
 #pragma unroll
     for (int k = 0; k < CPL; ++k) {
-      uint32_t lt[kGroup];
+      uint32_t lt[KB];
 #pragma unroll
-      for (int i = 0; i < kGroup; ++i) {
+      for (int i = 0; i < KB; ++i) {
         acc[k][1][i] += acc[k][0][i];
         acc[k][2][i] += acc[k][1][i];
         acc[k][3][i] += acc[k][2][i];
         lt[i] = acc[k][3][i];
       }
 #pragma unroll
-      for (int i = 0; i < kGroup; ++i) {
+      for (int i = 0; i < KB; ++i) {
         const uint32_t x = warp_scan_pred(lt[i]);
         const uint32_t ex = x - lt[i] + run[i];
 #pragma unroll
@@ -845,7 +856,12 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
         run[i] += __shfl_sync(kFull, x, 31);
       }
     }
-    if (lane == 0) tot[0][0][warp] = make_uint4(run[0], run[1], run[2], run[3]);
+    if (lane == 0) {
+      uint32_t r4[kGroup] = {};
+#pragma unroll
+      for (int i = 0; i < KB; ++i) r4[i] = run[i];
+      tot[0][0][warp] = make_uint4(r4[0], r4[1], r4[2], r4[3]);
+    }
     __syncthreads();
     const uint4 tw = lane < warp ? tot[0][0][lane] : make_uint4(0u, 0u, 0u, 0u);
     uint32_t wp[4] = {__reduce_add_sync(kFull, tw.x), __reduce_add_sync(kFull, tw.y),
@@ -862,7 +878,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int i = 0; i < kGroup; ++i) acc[k][j][i] += wp[i];
+        for (int i = 0; i < KB; ++i) acc[k][j][i] += wp[i];
     __syncthreads();  // tot[0] is reused by the first batch
   }
 
@@ -872,7 +888,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
   uint32_t* prow[CPL];
 #pragma unroll
   for (int k = 0; k < CPL; ++k) prow[k] = plane0 + rs * W + ct + cl[k];
-  const bool full_group = nbins_here == kGroup;
+  const bool full_group = nbins_here == KB;
   uint32_t* stage = STG ? reinterpret_cast<uint32_t*>(ring + (size_t)NST * R * a.TW) : nullptr;
   for (int b = nb_count; b < nb_total; ++b) {
     const int bi = b - nb_count;
@@ -881,14 +897,22 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     const int rows = (int)(re - r0 < R ? re - r0 : R);
     if (TMA) mbar_wait(&full_bar[b % NST], (uint32_t)((b / NST) & 1));
 
-    uint32_t v[R][CPL][4];  // packed in-chunk inclusive row prefix, 4 bins per word
-    uint32_t ct[R][CPL];    // packed chunk totals
+    uint32_t v[NP][CPL][4];  // packed in-chunk inclusive row prefix: byte q*KB+i = row q, bin i
+    uint32_t ct[NP][CPL];    // packed chunk totals
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) {
+    for (int rr = 0; rr < NP; ++rr) {  // packed pass rr: rows rr*KR .. rr*KR+KR-1
 #pragma unroll
       for (int k = 0; k < CPL; ++k) {
         uint32_t o[4] = {0u, 0u, 0u, 0u};
-        if (rr < rows) onehot4(b, rr, k, o);
+#pragma unroll
+        for (int q = 0; q < KR; ++q) {
+          if (rr * KR + q < rows) {
+            uint32_t oq[4];
+            onehot4(b, rr * KR + q, k, oq);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) o[j] += oq[j] << (8 * KB * q);
+          }
+        }
         const uint32_t l1 = o[0] + o[1];
         const uint32_t l2 = l1 + o[2];
         const uint32_t l3 = l2 + o[3];
@@ -920,41 +944,45 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
     __syncthreads();  // totals visible; every warp is done reading the ring stage
     if (TMA && threadIdx.x == 0 && b + NST < nb_total) issue(b + NST);
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) {
-      const uint4 tw = lane < warp ? tot[buf][rr][lane] : make_uint4(0u, 0u, 0u, 0u);
-      uint32_t run[kGroup] = {__reduce_add_sync(kFull, tw.x), __reduce_add_sync(kFull, tw.y),
-                              __reduce_add_sync(kFull, tw.z), __reduce_add_sync(kFull, tw.w)};
+    for (int pp = 0; pp < NP; ++pp) {
+      const uint4 tw = lane < warp ? tot[buf][pp][lane] : make_uint4(0u, 0u, 0u, 0u);
+      uint32_t run4[kGroup] = {__reduce_add_sync(kFull, tw.x), __reduce_add_sync(kFull, tw.y),
+                               __reduce_add_sync(kFull, tw.z), __reduce_add_sync(kFull, tw.w)};
       if (COLT && t > 0) {
-        const uint4 L = sleft[buf][rr];
-        run[0] += L.x;
-        run[1] += L.y;
-        run[2] += L.z;
-        run[3] += L.w;
+        const uint4 L = sleft[buf][pp];
+        run4[0] += L.x;
+        run4[1] += L.y;
+        run4[2] += L.z;
+        run4[3] += L.w;
       }
+#pragma unroll
+      for (int q = 0; q < KR; ++q) {
+      const int rr = pp * KR + q;  // the row of this batch
+      uint32_t* run = run4 + q * KB;  // this row's byte lanes
       if (rr < rows) {
 #pragma unroll
         for (int k = 0; k < CPL; ++k) {
 #pragma unroll
           for (int j = 0; j < 4; ++j)
 #pragma unroll
-            for (int i = 0; i < kGroup; ++i) acc[k][j][i] += run[i] + byte_of(v[rr][k][j], i);
+            for (int i = 0; i < KB; ++i) acc[k][j][i] += run[i] + byte_of(v[pp][k][j], q * KB + i);
 #pragma unroll
-          for (int i = 0; i < kGroup; ++i) run[i] += byte_of(ct[rr][k], i);
+          for (int i = 0; i < KB; ++i) run[i] += byte_of(ct[pp][k], q * KB + i);
           if (STG) {
-            uint32_t* sp = stage + (size_t)rr * kGroup * a.TW + cl[k];
+            uint32_t* sp = stage + (size_t)rr * KB * a.TW + cl[k];
 #pragma unroll
-            for (int i = 0; i < kGroup; ++i)
+            for (int i = 0; i < KB; ++i)
               *reinterpret_cast<uint4*>(sp + (size_t)i * a.TW) =
                   make_uint4(acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
           } else if (colok[k]) {
             uint32_t* p = prow[k];
             if (VEC && full_group) {
 #pragma unroll
-              for (int i = 0; i < kGroup; ++i, p += plane_elems)
+              for (int i = 0; i < KB; ++i, p += plane_elems)
                 st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
             } else {
 #pragma unroll
-              for (int i = 0; i < kGroup; ++i, p += plane_elems) {
+              for (int i = 0; i < KB; ++i, p += plane_elems) {
                 if (i < nbins_here) {
                   if (VEC) {
                     st_stream_v4(p, acc[k][0][i], acc[k][1][i], acc[k][2][i], acc[k][3][i]);
@@ -985,6 +1013,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
           prow[k] += W;
         }
       }
+      }  // q
     }
     if (STG) {  // the batch's rows are staged: bulk-copy whole plane rows out
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -995,7 +1024,7 @@ __global__ void __launch_bounds__(MAXT, COLT ? 2 : 0) k2_scan(ScanArgs a, RelLut
             uint32_t* dst = plane0 + (int64_t)i * plane_elems + (r0 + rr) * W;
             asm volatile(
                 "cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst),
-                "r"(smem_u32(stage + ((size_t)rr * kGroup + i) * a.TW)), "r"((uint32_t)(W * 4))
+                "r"(smem_u32(stage + ((size_t)rr * KB + i) * a.TW)), "r"((uint32_t)(W * 4))
                 : "memory");
           }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");

@@ -18,7 +18,7 @@ from paper_1711_01919_b200 import device  # noqa: E402
 KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY_CLUSTER",
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
          "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT",
-         "IH_STAGED_STORES", "IH_NO_RESTAGE")
+         "IH_STAGED_STORES", "IH_NO_RESTAGE", "IH_NO_ROWPACK")
 
 
 def _case(rng):

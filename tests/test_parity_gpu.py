@@ -26,7 +26,7 @@ def crc_of(t) -> str:
 @pytest.fixture(autouse=True)
 def _clean_env(monkeypatch):
     for k in ("IH_NSEG", "IH_ROWS_PER_BATCH", "IH_TARGET_WARPS", "IH_MIN_SEG_ROWS", "IH_NO_TMA",
-              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_CLUSTER", "IH_NO_RESTAGE"):
+              "IH_CARRY_LOOKBACK", "IH_TABLE_SUM_MAX", "IH_NO_COLTILE", "IH_NO_BIG", "IH_COLCOUNTS_SLAB", "IH_K4_MODE", "IH_K5_DIRECT", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_CLUSTER", "IH_NO_RESTAGE", "IH_NO_ROWPACK"):
         monkeypatch.delenv(k, raising=False)
 
 
@@ -650,3 +650,33 @@ def test_c7_device_count_determinism(rng, shard):
             for f in range(8):
                 assert np.array_equal(got[f], O.compute_crossweave(frames[f], lut, 37))
         assert np.array_equal(got, ref), g
+
+
+@pytest.mark.parametrize("rowpack", [True, False])
+def test_row_packed_one_and_two_bin_slabs(monkeypatch, rng, rowpack):
+    """1- and 2-bin slabs pack 4 / 2 rows into the byte lanes of a word (KB =
+    1 / 2); against the oracle with segments, tail splits, frame batches, odd
+    widths, LDG inputs and bin slabs of larger specs, and with IH_NO_ROWPACK."""
+    if not rowpack:
+        monkeypatch.setenv("IH_NO_ROWPACK", "1")
+    cases = [(1, 300, 1000, 1, None), (3, 97, 130, 2, None), (2, 257, 2048, 37, (5, 6)),
+             (1, 1080, 1920, 32, (30, 32)), (4, 33, 7, 2, None), (1, 1, 1, 1, None)]
+    for nseg, tail in [("0", None), ("5", "30"), ("3", None)]:
+        if nseg != "0":
+            monkeypatch.setenv("IH_NSEG", nseg)
+        else:
+            monkeypatch.delenv("IH_NSEG", raising=False)
+        if tail:
+            monkeypatch.setenv("IH_TAIL_PCT", tail)
+        else:
+            monkeypatch.delenv("IH_TAIL_PCT", raising=False)
+        for (F, h, w, bins, br) in cases:
+            frames = rng.integers(0, 256, (F, h, w + 3), dtype=np.uint8)
+            view = torch.from_numpy(frames).cuda()[:, :, 3:]
+            lut = O.np_uniform_table(bins)
+            lo, hi = br or (0, bins)
+            got = device.integral_histogram(view, lut, bins, bin_range=br,
+                                            kernel="single_pass").cpu().numpy()
+            for f in range(F):
+                want = O.compute_crossweave(np.ascontiguousarray(frames[f, :, 3:]), lut, bins)[lo:hi]
+                assert np.array_equal(got[f], want), (F, h, w, bins, br, nseg, tail, f)
