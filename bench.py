@@ -359,6 +359,41 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
             planes = gold[f"{wl.width}x{wl.height}x{wl.bins}"]["plane_crc"]
             crc_ok = f"{zlib.crc32(out[0, 0].cpu().numpy().tobytes()):08x}" == planes[b0]
 
+    # ---- cfg4's batched region queries (K3) on this rank's slab: Q = 65,536
+    # inclusive regions drawn as acceptance C4 does, timed apart
+    queries = None
+    if wl.key == "8k256" and active:
+        rng = np.random.default_rng(20260823 + 4)
+        Q = 65536
+        rr = np.sort(rng.integers(0, wl.height, (Q, 2)), axis=1)
+        cc = np.sort(rng.integers(0, wl.width, (Q, 2)), axis=1)
+        regs = torch.from_numpy(np.stack([rr[:, 0], cc[:, 0], rr[:, 1], cc[:, 1]], 1)
+                                .astype(np.int32)).to(dev)
+        slab = out[0]
+        res_q = torch.empty((Q, nb), dtype=torch.uint64, device=dev)
+        for _ in range(3):
+            device.region_histograms(slab, regs, out=res_q)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        e0.record()
+        for _ in range(10):
+            device.region_histograms(slab, regs, out=res_q)
+        e1.record()
+        torch.cuda.synchronize(dev)
+        q_ms = reduce_max([e0.elapsed_time(e1) / 10])[0]
+        # spot check against the four-corner formula on the host for a few queries
+        t_host = slab[:, :, :].view(torch.int32)
+        ok = True
+        for k in (0, 1, Q // 2, Q - 1):
+            r0, c0, r1, c1 = (int(x) for x in regs[k].tolist())
+            corners = [(r1, c1, 1), (r0 - 1, c1, -1), (r1, c0 - 1, -1), (r0 - 1, c0 - 1, 1)]
+            want = sum(sgn * t_host[:, a, b].to(torch.int64).remainder(1 << 32)
+                       for a, b, sgn in corners if a >= 0 and b >= 0)
+            ok = ok and bool(torch.equal(res_q[k].view(torch.int64).cpu(), want.cpu()))
+        queries = {"kernel": "k3_region_histograms", "Q": Q, "bins": nb, "ms": q_ms,
+                   "region_histograms_per_s": Q / (q_ms / 1e3), "spot_check": ok}
+        crc_ok = crc_ok and ok
+
     # ---- optional gather of bin slabs onto rank 0 (not part of the metric)
     gather_ms = None
     if args.gather and wl.shard == "bins" and world > 1:
@@ -431,6 +466,8 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     }
     if gather_ms is not None:
         line["gather_ms"] = gather_ms
+    if queries is not None:
+        line["queries"] = queries
     if e2e is not None:
         line["e2e"] = e2e
     if world == 1 and args.cpu_baseline:

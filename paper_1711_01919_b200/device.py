@@ -384,7 +384,7 @@ def _check_tensor(t: torch.Tensor) -> torch.Tensor:
     return t.contiguous()
 
 
-def region_histograms(t: torch.Tensor, regions, stream=None) -> torch.Tensor:
+def region_histograms(t: torch.Tensor, regions, stream=None, out=None) -> torch.Tensor:
     """Batched core.py:179-195: (Q, 4) inclusive (r0,c0,r1,c1) -> (Q, nb) uint64.
 
     Validation follows core.py:142 (degenerate) then core.py:158 (outside),
@@ -403,7 +403,11 @@ def region_histograms(t: torch.Tensor, regions, stream=None) -> torch.Tensor:
                 raise BoundsError(f"region outside {W}x{H} image")
         regs = torch.from_numpy(r.astype(np.int32)).to(t.device)
     Q = int(regs.shape[0])
-    out = torch.empty((Q, nb), dtype=torch.uint64, device=t.device)
+    if out is None:
+        out = torch.empty((Q, nb), dtype=torch.uint64, device=t.device)
+    elif out.shape != (Q, nb) or out.dtype not in (torch.uint64, torch.int64) or \
+            not out.is_contiguous() or out.device != t.device:
+        raise ShapeError(f"out must be a contiguous ({Q}, {nb}) uint64 tensor on {t.device}")
     if Q:
         with torch.cuda.device(t.device):
             _native.check(_native.lib().ih_region_histograms(

@@ -353,6 +353,10 @@ def test_c4_region_queries(rng):
             c0, c1 = sorted(rng.integers(0, w, 2).tolist())
             regs.append((r0, c0, r1, c1))
         got = ih.region_histogram_batch(t, regs)
+        dev_t = device.integral_histogram(device.upload_image(px), spec.table, bins)
+        pre = torch.empty((len(regs), bins), dtype=torch.uint64, device="cuda")
+        assert device.region_histograms(dev_t, regs, out=pre) is pre
+        assert np.array_equal(pre.cpu().numpy(), got)
         for k, (r0, c0, r1, c1) in enumerate(regs[:20]):
             one = ih.region_histogram(t, ih.Region(r0, c0, r1, c1)).counts
             assert np.array_equal(one, got[k])
