@@ -416,7 +416,13 @@ def region_histograms(t: torch.Tensor, regions, stream=None, out=None) -> torch.
     return out
 
 
-def window_counts(t: torch.Tensor, h: int, w: int, stream=None) -> torch.Tensor:
+def _check_out(out, shape, dtypes, dev):
+    if out.shape != shape or out.dtype not in dtypes or not out.is_contiguous() or out.device != dev:
+        raise ShapeError(f"out must be a contiguous {tuple(shape)} {dtypes[0]} tensor on {dev}")
+    return out
+
+
+def window_counts(t: torch.Tensor, h: int, w: int, stream=None, out=None) -> torch.Tensor:
     """likelihood.py:34-52 on the device -> (nb, H-h+1, W-w+1) int64."""
     if h < 1 or w < 1:
         raise ParameterError("window extents must be >= 1")
@@ -424,7 +430,9 @@ def window_counts(t: torch.Tensor, h: int, w: int, stream=None) -> torch.Tensor:
     nb, H, W = (int(x) for x in t.shape)
     if h > H or w > W:
         raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
-    out = torch.empty((nb, H - h + 1, W - w + 1), dtype=torch.int64, device=t.device)
+    shape = (nb, H - h + 1, W - w + 1)
+    out = torch.empty(shape, dtype=torch.int64, device=t.device) if out is None else \
+        _check_out(out, shape, (torch.int64,), t.device)
     with torch.cuda.device(t.device):
         _native.check(_native.lib().ih_window_counts(
             t.data_ptr(), nb, H, W, int(h), int(w), out.data_ptr(),
@@ -433,7 +441,7 @@ def window_counts(t: torch.Tensor, h: int, w: int, stream=None) -> torch.Tensor:
 
 
 def likelihood_map(t: torch.Tensor, template, h: int, w: int, metric: str = "bhattacharyya",
-                   stream=None) -> torch.Tensor:
+                   stream=None, out=None) -> torch.Tensor:
     """Fused K5 (likelihood.py:55-77): (H-h+1, W-w+1) float64 map on the device."""
     metrics = {"intersection": 0, "bhattacharyya": 1}
     if metric not in metrics:
@@ -447,7 +455,9 @@ def likelihood_map(t: torch.Tensor, template, h: int, w: int, metric: str = "bha
         raise ShapeError(f"template has {tmpl.shape} entries, tensor has {nb} bins")
     if h > H or w > W:
         raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
-    out = torch.empty((H - h + 1, W - w + 1), dtype=torch.float64, device=t.device)
+    shape = (H - h + 1, W - w + 1)
+    out = torch.empty(shape, dtype=torch.float64, device=t.device) if out is None else \
+        _check_out(out, shape, (torch.float64,), t.device)
     L = _native.lib()
     nws = int(L.ih_likelihood_workspace_bytes(nb, int(h), int(w)))
     with torch.cuda.device(t.device):
