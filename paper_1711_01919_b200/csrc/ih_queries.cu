@@ -8,6 +8,17 @@
 
 namespace ih {
 
+// A 32-bit read-only load whose L2 miss fetches 64 bytes from DRAM (instead
+// of the default 128): K3's corner reads are isolated, so half of a 128-byte
+// fetch is waste.  Measured (ncu, 65,536 regions x 32 bins): DRAM reads
+// 1.06 -> 0.53 GB per launch, time unchanged at 0.19 ms -- the gathers are
+// bound by request rate / latency, not by DRAM bandwidth.
+__device__ __forceinline__ uint32_t ldg_l2_64(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.L2::64B.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
 // K3: one warp per query (grid-stride over queries), lanes over bins: the
 // (Q, nb) u64 output row of a query is written coalesced, and each lane keeps
 // 4 corners x 4 bins = 16 independent gathers in flight (the reads are random
@@ -36,10 +47,10 @@ __global__ void __launch_bounds__(256) k3_region_histograms(const uint32_t* __re
       for (int u = 0; u < 4; ++u) {
         const int b = b0 + u * 32 + lane;
         const uint32_t* p = t + (int64_t)(b < nb ? b : 0) * plane;
-        v[u][0] = b < nb ? __ldg(p + o11) : 0u;
-        v[u][1] = b < nb && top ? __ldg(p + o01) : 0u;
-        v[u][2] = b < nb && left ? __ldg(p + o10) : 0u;
-        v[u][3] = b < nb && top && left ? __ldg(p + o00) : 0u;
+        v[u][0] = b < nb ? ldg_l2_64(p + o11) : 0u;
+        v[u][1] = b < nb && top ? ldg_l2_64(p + o01) : 0u;
+        v[u][2] = b < nb && left ? ldg_l2_64(p + o10) : 0u;
+        v[u][3] = b < nb && top && left ? ldg_l2_64(p + o00) : 0u;
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
