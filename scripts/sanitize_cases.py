@@ -9,15 +9,17 @@ from paper_1711_01919_b200 import device
 
 rng = np.random.default_rng(7)
 cases = [(1, 1, 3), (7, 131, 5), (61, 257, 16), (100, 300, 64), (33, 2049, 7), (40, 4100, 9), (9, 8192, 4),
-         (21, 10001, 256), (70, 3840, 128)]
+         (21, 10001, 256), (70, 3840, 128), (50, 1921, 1), (45, 1922, 2), (30, 701, 2)]
 envs = [{}, {"IH_NSEG": "3"}, {"IH_NSEG": "5", "IH_TABLE_SUM_MAX": "1"},
         {"IH_NSEG": "4", "IH_CARRY_LOOKBACK": "1"}, {"IH_NO_TMA": "1", "IH_NSEG": "2"},
         {"IH_ROWS_PER_BATCH": "1", "IH_NSEG": "3"}, {"IH_NSEG": "6", "IH_COLCOUNTS_SLAB": "1"},
-        {"IH_NSEG": "3", "IH_NO_COLTILE": "1"}]
+        {"IH_NSEG": "3", "IH_NO_COLTILE": "1"}, {"IH_NSEG": "4", "IH_TAIL_PCT": "30"},
+        {"IH_NSEG": "3", "IH_CARRY_CLUSTER": "1"}, {"IH_NSEG": "2", "IH_STAGED_STORES": "1"}]
 bad = 0
 for env in envs:
     for k in ("IH_NSEG", "IH_TABLE_SUM_MAX", "IH_CARRY_LOOKBACK", "IH_NO_TMA", "IH_ROWS_PER_BATCH",
-              "IH_COLCOUNTS_SLAB", "IH_NO_COLTILE"):
+              "IH_COLCOUNTS_SLAB", "IH_NO_COLTILE", "IH_TAIL_PCT", "IH_CARRY_CLUSTER",
+              "IH_STAGED_STORES"):
         os.environ.pop(k, None)
     os.environ.update(env)
     for (h, w, b) in cases:
