@@ -114,16 +114,23 @@ struct K2Plan {
 // shared memory above 48 KB needs the attribute, so it is set for any
 // non-zero request (once per kernel and size: cached).
 bool set_dyn_smem(const void* fn, size_t bytes) {
+  // the attribute is per device: cache by (kernel, current device)
   static std::mutex mu;
-  static std::unordered_map<const void*, size_t> done;
+  static std::unordered_map<uint64_t, size_t> done;
   if (bytes == 0) return true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const uint64_t key = (uint64_t)(uintptr_t)fn * 64u + (uint64_t)dev;
   std::lock_guard<std::mutex> lock(mu);
-  auto it = done.find(fn);
+  auto it = done.find(key);
   if (it != done.end() && it->second >= bytes) return true;
   if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes) !=
       cudaSuccess)
     return false;
-  done[fn] = bytes;
+  done[key] = bytes;
   return true;
 }
 
