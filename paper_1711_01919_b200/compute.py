@@ -8,9 +8,9 @@ the four ``compute_*`` functions with their signatures and validation order.
 Every strategy runs on the device and returns the identical tensor (the
 reference's contract):
 
-  sequential / sts / wavefront -> K2, the single-pass tiled 2D scan
-  crossweave                   -> K1 + K1b, the paper's CW-B on the GPU
-                                  (fused bin + row scan, then column scan)
+  every strategy -> K2, the single-pass tiled 2D scan (the paper's CW-B on
+  the GPU, K1 + K1b, is 3-4x slower and stays available as
+  device.integral_histogram(kernel="crossweave"))
 
 ``workers`` is validated (ParameterError when negative, strategies.py:62-65)
 and otherwise has no effect: device parallelism is fixed by the kernels.
@@ -33,11 +33,17 @@ DEFAULT_TILE = 64  # strategies.py:34 (wavefront tile side; a schedule hint here
 STRATEGY_NAMES = ("sequential", "crossweave", "sts", "wavefront")
 
 # strategy name -> kernel family of the C ABI (include/inthist_b200.h ih_kernel)
+# Every strategy runs the single pass: on the device they are one computation
+# (the reference's strategies differ only in CPU parallelisation),
+# and the paper's cross-weave kernels (K1 + K1b, 3-4x the output traffic) are
+# 3-4x slower -- a caller who picks crossweave as the reference's fastest CPU
+# path should not get the slowest device path.  K1 + K1b stay reachable as
+# kernel="crossweave" (device API) / IH_KERNEL_CROSSWEAVE (C ABI).
 _KERNEL_OF = {
     "sequential": "auto",
     "sts": "auto",
     "wavefront": "auto",
-    "crossweave": "crossweave",
+    "crossweave": "auto",
 }
 
 
@@ -88,7 +94,8 @@ def compute_sequential(img: GrayImage, spec: BinSpec) -> IntegralHistogram:
 
 
 def compute_crossweave(img: GrayImage, spec: BinSpec, workers: int = 0) -> IntegralHistogram:
-    """CW-B (strategies.py:129-150): capacity, then workers, then K1 + K1b."""
+    """CW-B (strategies.py:129-150): capacity, then workers, then the device pass
+    (the single pass; K1 + K1b via device.integral_histogram(kernel="crossweave"))."""
     img.check_capacity()
     resolve_workers(workers)
     return _on_device(img, spec, _KERNEL_OF["crossweave"])
