@@ -140,3 +140,27 @@ def test_plan_hint_overrides_segments():
     assert device.plan(8, 1080, 1920, 32)["segments"] == base
     cands = device.segment_candidates(8, 1080, 1920, 32)
     assert base in cands and all(1 <= n <= 34 for n in cands)
+
+
+def test_plan_variants_on_cpu(monkeypatch):
+    """Planner decisions that need no device: row packing for 1-/2-bin slabs,
+    tail splits from hints, hint validation."""
+    from paper_1711_01919_b200 import device
+    from paper_1711_01919_b200.errors import ParameterError as PE
+
+    p1 = device.plan(64, 1080, 1920, 1)
+    p4 = device.plan(64, 1080, 1920, 4)
+    assert p1["workspace_bytes"] * 4 == p4["workspace_bytes"]  # KB = 1: nbp = 1 (not 4)
+    monkeypatch.setenv("IH_NO_ROWPACK", "1")
+    assert device.plan(64, 1080, 1920, 1)["workspace_bytes"] == p4["workspace_bytes"]
+    monkeypatch.delenv("IH_NO_ROWPACK")
+    device.set_plan_hint(4, 1000, 700, 9, 6, 30, 4)
+    try:
+        p = device.plan(4, 1000, 700, 9)
+        assert p["big_segments"] < p["segments"] and p["tail_segment_rows"] * 4 >= p["segment_rows"] - 3
+    finally:
+        device.set_plan_hint(4, 1000, 700, 9, 0)
+    with pytest.raises(PE):
+        device.set_plan_hint(4, 1000, 700, 9, 6, 120, 4)
+    with pytest.raises(PE):
+        device.set_plan_hint(4, 1000, 700, 9, -1)
