@@ -684,3 +684,14 @@ def test_row_packed_one_and_two_bin_slabs(monkeypatch, rng, rowpack):
             for f in range(F):
                 want = O.compute_crossweave(np.ascontiguousarray(frames[f, :, 3:]), lut, bins)[lo:hi]
                 assert np.array_equal(got[f], want), (F, h, w, bins, br, nseg, tail, f)
+
+
+def test_tall_and_wide_column_tiles(rng):
+    """H > 65535 with column tiles: u16 prefix tables are impossible, the scan
+    sums count slots, and every tile adds row carries and chunk totals."""
+    px = rng.integers(0, 256, (70001, 2100), dtype=np.uint8)
+    lut = O.np_uniform_table(2)
+    assert device.plan(1, 70001, 2100, 2)["column_tiles"] == 2
+    got = dev_compute(px, lut, 2, kernel="single_pass")
+    want = O.compute_crossweave(px, lut, 2)
+    assert np.array_equal(got.cpu().numpy(), want)
