@@ -729,12 +729,27 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   if (!t || !out) return fail(IH_ERR_PARAM, "null pointer");
   if (nb > 65535) return fail(IH_ERR_PARAM, "too many bins");
   const int64_t R = height - h + 1, C = width - w + 1;
-  // IH_K4_MODE: 1 (default) four-corner gathers, 4 outputs per thread;
-  // 2 staged row differences while CW + w u32 fit in shared memory; 0 the
-  // two-output four-corner kernel
   const int threads = C >= 1024 ? 256 : (int)((C + 127) / 128 * 32);
   const size_t smem = (size_t)(4 * threads + w) * sizeof(uint32_t);
-  const int64_t k4mode = env_int("IH_K4_MODE", 1);  // 0 corners, 1 ILP corners, 2 staged
+  // IH_K4_MODE 3 (default): pairs of adjacent outputs per 16-byte store;
+  // 1: 4 strided outputs per thread; 0: the two-output kernel; 2: staged row
+  // differences (while CW + w u32 fit in shared memory)
+  const int64_t k4mode = env_int("IH_K4_MODE", 3);
+  if (k4mode == 3) {  // two adjacent outputs per 16-byte store
+    const int U = env_int("IH_K4_PAIRS_U", 2) == 4 ? 4 : env_int("IH_K4_PAIRS_U", 2) == 1 ? 1 : 2;
+    const int64_t cb = (C + 1 + 2 * 256 * U - 1) / (2 * 256 * U);  // U pairs per thread
+    // grid-strided rows, ~256 CTAs' worth per SM (measured best: HD x32 64x64
+    // windows 0.164 -> 0.148 ms vs mode 1; profiles/r01f/queries_k4_pairs.jsonl)
+    int64_t ry = (int64_t)kNumSMs * env_int("IH_K4_CTAS_PER_SM", 256) / (cb * nb);
+    ry = ry < 1 ? 1 : ry > R ? R : ry > 65535 ? 65535 : ry;
+    dim3 grid((unsigned)cb, (unsigned)ry, (unsigned)nb);
+    auto k = U == 4 ? ih::k4_window_counts_pairs<4> : U == 1 ? ih::k4_window_counts_pairs<1>
+                                                            : ih::k4_window_counts_pairs<2>;
+    k<<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h, w,
+                                             reinterpret_cast<long long*>(out));
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts_pairs");
+    return IH_OK;
+  }
   if (k4mode == 1) {
     // rows are grid-strided over ~64 CTAs per SM in total, so each CTA walks
     // several rows (one-row CTAs: 0.52 of HBM, 148*64 CTAs: 0.59, HD x32;

@@ -125,6 +125,52 @@ __global__ void __launch_bounds__(256, MINB) k4_window_counts_ilp(const uint32_t
   }
 }
 
+// K4 (pairs): like k4_window_counts_ilp, but a thread forms two adjacent
+// outputs per step and writes them with one 16-byte streaming store.  The pair
+// start is shifted by the parity of the row's first element index, so every
+// pair store is 16-byte aligned for any output width; column 0 of an odd-based
+// row is stored alone.
+template <int U>
+__global__ void __launch_bounds__(256, 6) k4_window_counts_pairs(const uint32_t* __restrict__ t,
+                                                                  int nb, int64_t H, int64_t W,
+                                                                  int h, int w,
+                                                                  long long* __restrict__ out) {
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const int64_t b = blockIdx.z;
+  const uint32_t* p = t + b * H * W;
+  for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
+    const uint32_t* bot = p + (i + h - 1) * W;
+    const uint32_t* topr = p + (i - 1) * W;  // used only when i > 0
+    const int64_t rowbase = (b * R + i) * C;
+    long long* orow = out + rowbase;
+    const int off = (int)(rowbase & 1);  // pairs start at odd columns when rowbase is odd
+    auto count = [&](int64_t j) -> uint32_t {
+      const uint32_t a11 = __ldg(bot + j + w - 1);
+      const uint32_t a10 = j > 0 ? __ldg(bot + j - 1) : 0u;
+      const uint32_t a01 = i > 0 ? __ldg(topr + j + w - 1) : 0u;
+      const uint32_t a00 = i > 0 && j > 0 ? __ldg(topr + j - 1) : 0u;
+      return a11 - a10 - a01 + a00;  // exact in u32
+    };
+    uint32_t n[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t js = 2 * (((int64_t)blockIdx.x * U + u) * blockDim.x + threadIdx.x) + off;
+      n[u][0] = js < C ? count(js) : 0u;
+      n[u][1] = js + 1 < C ? count(js + 1) : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t js = 2 * (((int64_t)blockIdx.x * U + u) * blockDim.x + threadIdx.x) + off;
+      if (js + 1 < C)
+        __stcs(reinterpret_cast<longlong2*>(orow + js),
+               make_longlong2((long long)n[u][0], (long long)n[u][1]));
+      else if (js < C)
+        __stcs(orow + js, (long long)n[u][0]);
+    }
+    if (off && blockIdx.x == 0 && threadIdx.x == 0) __stcs(orow, (long long)count(0));
+  }
+}
+
 // Row-difference staging for K4 (the "vs" variant).  For output
 // row i the window count at column j is
 //     V[j + w - 1] - V[j - 1],   V(c) = T(i + h - 1, c) - T(i - 1, c)

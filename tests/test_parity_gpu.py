@@ -502,7 +502,7 @@ def test_window_count_kernel_variants(monkeypatch, rng):
         t = torch.from_numpy(full.view(np.int32)).cuda().view(torch.uint32)
         for (h, w) in [(1, 1), (min(5, H), min(8, W)), (H, W), (H // 2 + 1, W // 3 + 1), (1, W), (H, 1)]:
             want = O.window_counts(full, h, w)
-            for mode in ("0", "1", "2"):
+            for mode in ("0", "1", "2", "3"):
                 monkeypatch.setenv("IH_K4_MODE", mode)
                 assert np.array_equal(device.window_counts(t, h, w).cpu().numpy(), want), (H, W, h, w, mode)
 
