@@ -345,4 +345,71 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tab(const uint32_t* __r
   }
 }
 
+// K5 (table, P adjacent placements per thread): each bin's four corner
+// pointers serve P placements (loads at +0..+P-1): a P-th of the address
+// arithmetic per placement.  Same terms, same bin order: bit-identical to
+// k5_likelihood_map / _tab.
+template <int P>
+__global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __restrict__ t, int nb,
+                                                               int64_t H, int64_t W, int h, int w,
+                                                               const double* __restrict__ M,
+                                                               double* __restrict__ out) {
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const int64_t n1 = (int64_t)h * w + 1;
+  const int64_t plane = H * W;
+  for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
+    const int64_t j = P * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    if (j >= C) continue;
+    const int64_t o11 = (i + h - 1) * W + (j + w - 1);
+    const int64_t o01 = (i - 1) * W + (j + w - 1);
+    const int64_t o10 = (i + h - 1) * W + (j - 1);
+    const int64_t o00 = (i - 1) * W + (j - 1);
+    bool ok[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) ok[q] = j + q < C;
+    double acc[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) acc[q] = 0.0;
+    constexpr int U = P >= 4 ? 2 : 4;  // bins per step
+    for (int b0 = 0; b0 < nb; b0 += U) {
+      uint32_t n[U][P];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u < nb ? b0 + u : nb - 1;
+        const uint32_t* p = t + (int64_t)b * plane;
+        const uint32_t* p11 = p + o11;
+        const uint32_t* p10 = p + o10;
+        const uint32_t* p01 = p + o01;
+        const uint32_t* p00 = p + o00;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const bool left = j + q > 0;
+          const uint32_t a11 = ok[q] ? __ldg(p11 + q) : 0u;
+          const uint32_t a10 = ok[q] && left ? __ldg(p10 + q) : 0u;
+          const uint32_t a01 = ok[q] && i > 0 ? __ldg(p01 + q) : 0u;
+          const uint32_t a00 = ok[q] && i > 0 && left ? __ldg(p00 + q) : 0u;
+          n[u][q] = a11 - a10 - a01 + a00;  // exact window count
+        }
+      }
+      double m[U][P];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int b = b0 + u < nb ? b0 + u : nb - 1;
+        const double* Mb = M + (int64_t)b * n1;
+#pragma unroll
+        for (int q = 0; q < P; ++q) m[u][q] = ok[q] ? __ldg(Mb + n[u][q]) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u)  // the sum over bins stays in order b = 0..nb-1
+        if (b0 + u < nb) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) acc[q] += m[u][q];
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < P; ++q)
+      if (ok[q]) out[i * C + j + q] = fmin(fmax(acc[q], 0.0), 1.0);
+  }
+}
+
 }  // namespace ih

@@ -522,6 +522,11 @@ def test_likelihood_table_path_bit_identical(monkeypatch, rng):
                 monkeypatch.setenv("IH_K5_DIRECT", "1")
                 b = device.likelihood_map(t, tmpl, h, w, m).cpu().numpy()
                 assert np.array_equal(a.view(np.int64), b.view(np.int64)), (H, W, B, h, w, m)
+                monkeypatch.delenv("IH_K5_DIRECT")
+                monkeypatch.setenv("IH_K5_PAIRS", "0")  # one placement per thread
+                c = device.likelihood_map(t, tmpl, h, w, m).cpu().numpy()
+                monkeypatch.delenv("IH_K5_PAIRS")
+                assert np.array_equal(a.view(np.int64), c.view(np.int64)), (H, W, B, h, w, m)
 
 
 @pytest.mark.parametrize("metric", ["intersection", "bhattacharyya"])
