@@ -149,6 +149,38 @@ def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments
                                              int(tail_pct), int(tail_div), 1 if cluster else 0))
 
 
+_TUNED: dict = {}  # (frames, H, W, slab_bins) -> (segments, tail_pct, tail_div), this process
+
+
+def save_tuning(path: str) -> int:
+    """Write this process's autotune results (plan hints) to a JSON file, keyed
+    by the GPU model and the ABI version; returns the number of entries."""
+    import json
+
+    name = torch.cuda.get_device_name(0) if torch.cuda.is_available() else "none"
+    doc = {"gpu": name, "abi": int(_native.lib().ih_abi_version()),
+           "hints": [list(k) + list(v) for k, v in sorted(_TUNED.items())]}
+    with open(path, "w") as fh:
+        json.dump(doc, fh, indent=1)
+    return len(_TUNED)
+
+
+def load_tuning(path: str) -> int:
+    """Apply plan hints saved by save_tuning (skipped, returning 0, when they
+    were measured on another GPU model or ABI version)."""
+    import json
+
+    with open(path) as fh:
+        doc = json.load(fh)
+    name = torch.cuda.get_device_name(0) if torch.cuda.is_available() else "none"
+    if doc.get("gpu") != name or doc.get("abi") != int(_native.lib().ih_abi_version()):
+        return 0
+    for frames, height, width, nb, segs, tail_pct, tail_div in doc["hints"]:
+        set_plan_hint(frames, height, width, nb, segs, tail_pct, tail_div)
+        _TUNED[(frames, height, width, nb)] = (segs, tail_pct, tail_div)
+    return len(doc["hints"])
+
+
 def segment_candidates(frames: int, height: int, width: int, slab_bins: int) -> list:
     """Row-segment counts worth measuring for a shape: the heuristic's choice and
     the counts whose scan grid ends just at (or just below) a whole number of
@@ -247,6 +279,7 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
                     times[(n0, tail_pct, 4)] = measure(n0, tail_pct, 4)
     best = min(times, key=times.get)
     set_plan_hint(frames, height, width, nb, *best)
+    _TUNED[(frames, height, width, nb)] = tuple(best)
     return {"segments": best[0], "tail_pct": best[1], "tail_div": best[2],
             "ms": {f"{k[0]}" + (f"/t{k[1]}" if k[1] else ""): round(v, 4) for k, v in times.items()}}
 

@@ -472,6 +472,22 @@ def test_autotune_pins_a_measured_segment_count(rng):
         device.set_plan_hint(3, 300, 700, 12, 0)
 
 
+def test_tuning_save_and_load(tmp_path):
+    """autotune results persist across processes: save_tuning / load_tuning
+    (keyed by GPU model and ABI version)."""
+    res = device.autotune(2, 200, 300, 7)
+    path = str(tmp_path / "tune.json")
+    try:
+        assert device.save_tuning(path) >= 1
+        want = device.plan(2, 200, 300, 7)
+        device.set_plan_hint(2, 200, 300, 7, 0)
+        assert device.load_tuning(path) >= 1
+        assert device.plan(2, 200, 300, 7) == want
+        assert want["big_segments"] >= 1 and res["segments"] >= 1
+    finally:
+        device.set_plan_hint(2, 200, 300, 7, 0)
+
+
 def test_plan_describe_matches_launches():
     p = device.plan(64, 1080, 1920, 32)
     assert p["kernel"] == "single_pass" and p["launches"] in (1, 2, 3)
