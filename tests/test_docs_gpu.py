@@ -1,4 +1,4 @@
-"""The reference-side ctypes stub documented in INTEGRATION.md §2, executed
+"""Documentation that runs: the reference-side ctypes stub of INTEGRATION.md §2, executed
 verbatim (its relative imports pointed at this package's mirror types and its
 library path at the in-tree .so) against the oracle."""
 
@@ -33,3 +33,15 @@ def test_integration_ctypes_stub_runs():
         spec = ih.BinSpec.uniform(b)
         got = ns["compute_sequential"](img, spec).counts
         assert np.array_equal(got, O.compute_crossweave(img.pixels, spec.table, b)), (h, w, b)
+
+
+@pytest.mark.parametrize("doc", ["README.md", "INTEGRATION.md"])
+def test_drop_in_snippets_run(doc):
+    """The drop-in snippets of README.md and INTEGRATION.md §1 run as written."""
+    text = open(os.path.join(ROOT, doc)).read()
+    code = re.search(r"```python\n(import paper_1711_01919_b200 as inthist.*?)```", text, re.S).group(1)
+    pixels = np.random.default_rng(1).integers(0, 256, (120, 200), dtype=np.uint8)
+    ns = {"pixels_u8": pixels}
+    exec(compile(code, doc, "exec"), ns)
+    want = O.brute_region_counts(pixels, O.np_uniform_table(32), 32, 10, 20, 59, 99)
+    assert np.array_equal(ns["h"].counts, want)
