@@ -167,6 +167,39 @@ ih_status ih_likelihood_map_ws(const uint32_t *t, int32_t nb, int64_t height, in
                                double *out, void *workspace, size_t workspace_bytes,
                                void *stream);
 
+/* --- Scan building blocks (reference scan.py:33-103), K6 kernels ----------
+ * Device pointers, asynchronous on `stream`; not on the integral-histogram
+ * path (K2 fuses its scans).
+ *
+ * ih_scan_u64: out[i] = in[0] + ... + in[i]  (exclusive = 0; scan.py:33-36)
+ *              out[i] = in[0] + ... + in[i-1] (exclusive = 1; scan.py:39-44)
+ * over n u64 elements, summed mod 2^64 like numpy's uint64 cumsum, stored as
+ * u32.  If any stored prefix exceeds 2^32-1 the kernels set *overflow to 1
+ * (it is cleared first; NULL skips the check) -- the caller raises the
+ * reference's ScanOverflowError after synchronising (scan.py:27-30).  The
+ * result equals the reference's blocked_scan for every block length
+ * (scan.py:47-76), whose three phases these kernels are.
+ * `workspace` (device, >= ih_scan_workspace_bytes(n), 8-byte aligned) holds
+ * the per-tile totals.  IH_ERR_PARAM: n < 0, null pointers, short workspace. */
+size_t ih_scan_workspace_bytes(int64_t n);
+ih_status ih_scan_u64(const uint64_t *in, int64_t n, uint32_t *out, int32_t exclusive,
+                      uint32_t *overflow, void *workspace, size_t workspace_bytes,
+                      void *stream);
+
+/* Inclusive u32 (wrapping) scan along the middle axis of a contiguous
+ * (outer, n, inner) array (numpy cumsum(dtype=uint32) semantics, scan.py:79-92):
+ * scan_rows of an (R, C) plane is (R, C, 1), scan_cols is (1, R, C).
+ * elem_bytes: 1 (u8 input) or 4 (u32 input); out is u32, same extents and
+ * not overlapping `in`.  IH_ERR_PARAM on bad extents / element size. */
+ih_status ih_scan_axis_u32(const void *in, int32_t elem_bytes, int64_t outer, int64_t n,
+                           int64_t inner, uint32_t *out, void *stream);
+
+/* out (cols x rows) = in (rows x cols)^T for elem_bytes in {1, 2, 4, 8, 16}
+ * (scan.py:95-103; the reference's cache-blocking tile is a host concern).
+ * IH_ERR_PARAM on bad extents / element size. */
+ih_status ih_transpose(const void *in, int64_t rows, int64_t cols, int32_t elem_bytes,
+                       void *out, void *stream);
+
 /* Debug: when set, k2_scan writes {start ns, prologue-done ns, end ns, SM id}
  * (4 u64) per CTA into the device buffer (grids of at most `ctas` CTAs).
  * NULL turns it off.  Not for production use (adds a barrier per CTA). */

@@ -7,7 +7,8 @@ relative to the reference package ``pkg/src/inthist/``):
   recursion (strategies.py:86-115), the threaded cross-weave
   (strategies.py:118-150), region queries (core.py:179-195), window counts
   (likelihood.py:34-52) and the streamed per-plane crc32 (streaming.py:123-155).
-* numpy restatements of the same functions, used to cross-check the C code.
+* numpy restatements of the same functions, used to cross-check the C code,
+  and of the scan module (scan.py:20-92; pinned by tests/golden/scans.npz).
 
 Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
 leg may import this module.  The product package never does; it has no CPU
@@ -198,3 +199,45 @@ def synth_image(width: int, height: int, seed: int) -> np.ndarray:
     """bench.py:59-62 -- deterministic uniform u8 image for (seed, W, H)."""
     rng = np.random.default_rng(np.random.SeedSequence([seed, width, height]))
     return rng.integers(0, 256, size=(height, width), dtype=np.uint8)
+
+
+class ScanOverflow(ArithmeticError):
+    """A 1-D prefix above 2^32-1 (the reference raises ScanOverflowError, scan.py:27-30)."""
+
+
+def _np_u32_prefixes(sums: np.ndarray) -> np.ndarray:
+    if sums.size and int(sums.max()) > 0xFFFF_FFFF:
+        raise ScanOverflow("prefix sum exceeds 32-bit range")
+    return sums.astype(np.uint32)
+
+
+def np_inclusive_scan(seq) -> np.ndarray:
+    """scan.py:20-36 restated: elements as uint64 (mod 2^64 sums), u32 result."""
+    v = np.asarray(seq).astype(np.uint64).reshape(-1)
+    return _np_u32_prefixes(np.cumsum(v, dtype=np.uint64))
+
+
+def np_exclusive_scan(seq) -> np.ndarray:
+    """scan.py:39-44 restated: the inclusive prefixes shifted right by one."""
+    v = np.asarray(seq).astype(np.uint64).reshape(-1)
+    sums = np.concatenate([np.zeros(1, np.uint64), np.cumsum(v, dtype=np.uint64)])[:v.size]
+    return _np_u32_prefixes(sums)
+
+
+def np_blocked_scan(seq, block: int) -> np.ndarray:
+    """scan.py:47-76 restated with explicit phases (block >= 1): per-block
+    prefixes, exclusive scan of block totals, offset add."""
+    v = np.asarray(seq).astype(np.uint64).reshape(-1)
+    if v.size == 0:
+        return np.zeros(0, np.uint32)
+    pad = (-v.size) % block
+    blocks = np.concatenate([v, np.zeros(pad, np.uint64)]).reshape(-1, block)
+    local = np.cumsum(blocks, axis=1, dtype=np.uint64)
+    offs = np.cumsum(local[:, -1], dtype=np.uint64) - local[:, -1]
+    return _np_u32_prefixes((local + offs[:, None]).reshape(-1)[:v.size])
+
+
+def np_scan_axis(plane, axis: int) -> np.ndarray:
+    """scan.py:79-92 restated: per-element u32 cast, wrapping u32 prefix along axis."""
+    a = np.asarray(plane)
+    return np.cumsum(a.astype(np.uint32), axis=axis, dtype=np.uint32)

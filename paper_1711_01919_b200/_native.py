@@ -41,6 +41,10 @@ EXPORTS = (
     "ih_debug_trace",
     "ih_likelihood_map_ws",
     "ih_likelihood_workspace_bytes",
+    "ih_scan_workspace_bytes",
+    "ih_scan_u64",
+    "ih_scan_axis_u32",
+    "ih_transpose",
     "ih_status_string",
     "ih_last_error",
     "ih_abi_version",
@@ -85,6 +89,14 @@ def lib() -> ctypes.CDLL:
     L.ih_likelihood_map_ws.restype = ctypes.c_int
     L.ih_likelihood_workspace_bytes.argtypes = [i32, i32, i32]
     L.ih_likelihood_workspace_bytes.restype = ctypes.c_size_t
+    L.ih_scan_workspace_bytes.argtypes = [i64]
+    L.ih_scan_workspace_bytes.restype = sz
+    L.ih_scan_u64.argtypes = [P, i64, P, i32, P, P, sz, P]
+    L.ih_scan_u64.restype = ctypes.c_int
+    L.ih_scan_axis_u32.argtypes = [P, i32, i64, i64, i64, P, P]
+    L.ih_scan_axis_u32.restype = ctypes.c_int
+    L.ih_transpose.argtypes = [P, i64, i64, i32, P, P]
+    L.ih_transpose.restype = ctypes.c_int
     L.ih_plan_describe.argtypes = [i64, i64, i64, i32, i32, i32, P]
     L.ih_plan_describe.restype = ctypes.c_int
     L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32, i32, i32, i32]

@@ -13,6 +13,7 @@
 #include "../../include/inthist_b200.h"
 #include "ih_kernels.cuh"
 #include "ih_queries.cu"
+#include "ih_scan.cu"
 #include "ih_single_pass.cu"
 
 namespace {
@@ -922,6 +923,99 @@ ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t sl
   return IH_OK;
 }
 
+size_t ih_scan_workspace_bytes(int64_t n) {
+  const int64_t tiles = n > 0 ? (n + ih::kScanTile - 1) / ih::kScanTile : 0;
+  return (size_t)(tiles > 0 ? tiles : 1) * sizeof(uint64_t);
+}
+
+ih_status ih_scan_u64(const uint64_t* in, int64_t n, uint32_t* out, int32_t exclusive,
+                      uint32_t* overflow, void* workspace, size_t workspace_bytes, void* stream) {
+  if (n < 0) return fail(IH_ERR_PARAM, "n must be >= 0");
+  if (n == 0) return IH_OK;
+  if (!in || !out || !workspace) return fail(IH_ERR_PARAM, "null pointer");
+  if (workspace_bytes < ih_scan_workspace_bytes(n) || ((uintptr_t)workspace & 7))
+    return fail(IH_ERR_PARAM, "scan workspace too small or misaligned");
+  const int64_t tiles = (n + ih::kScanTile - 1) / ih::kScanTile;
+  if (tiles > 0x7fffffffLL) return fail(IH_ERR_PARAM, "n too large");
+  cudaStream_t s = (cudaStream_t)stream;
+  uint64_t* totals = static_cast<uint64_t*>(workspace);
+  const bool v2 = ((uintptr_t)in & 15) == 0, v4 = ((uintptr_t)out & 15) == 0;
+  const dim3 grid((unsigned)tiles);
+  if (v2)
+    ih::k6_block_totals<true><<<grid, ih::kScanThreads, 0, s>>>(in, n, totals);
+  else
+    ih::k6_block_totals<false><<<grid, ih::kScanThreads, 0, s>>>(in, n, totals);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k6_block_totals");
+  ih::k6_scan_totals<<<1, ih::kScanThreads, 0, s>>>(totals, tiles, overflow);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k6_scan_totals");
+  auto k = v2 ? (v4 ? ih::k6_scan_apply<true, true> : ih::k6_scan_apply<true, false>)
+              : (v4 ? ih::k6_scan_apply<false, true> : ih::k6_scan_apply<false, false>);
+  k<<<grid, ih::kScanThreads, 0, s>>>(in, n, totals, exclusive ? 1 : 0, out, overflow);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k6_scan_apply");
+  return IH_OK;
+}
+
+ih_status ih_scan_axis_u32(const void* in, int32_t elem_bytes, int64_t outer, int64_t n,
+                           int64_t inner, uint32_t* out, void* stream) {
+  if (outer < 0 || n < 0 || inner < 0) return fail(IH_ERR_PARAM, "extents must be >= 0");
+  if (elem_bytes != 1 && elem_bytes != 4) return fail(IH_ERR_PARAM, "elem_bytes must be 1 or 4");
+  if (outer == 0 || n == 0 || inner == 0) return IH_OK;
+  if (!in || !out) return fail(IH_ERR_PARAM, "null pointer");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (inner == 1) {
+    const int64_t blocks = (outer + 7) / 8;
+    if (blocks > 0x7fffffffLL) return fail(IH_ERR_PARAM, "too many rows");
+    // vector path: every row start 16-byte aligned (u32) / 4-byte aligned (u8)
+    const bool vec = n % 4 == 0 && ((uintptr_t)in % (elem_bytes * 4)) == 0 &&
+                     ((uintptr_t)out & 15) == 0;
+    const unsigned g = (unsigned)blocks;
+    if (elem_bytes == 1) {
+      auto k = vec ? ih::k6_scan_inner<uint8_t, true> : ih::k6_scan_inner<uint8_t, false>;
+      k<<<g, 256, 0, s>>>(static_cast<const uint8_t*>(in), outer, n, out);
+    } else {
+      auto k = vec ? ih::k6_scan_inner<uint32_t, true> : ih::k6_scan_inner<uint32_t, false>;
+      k<<<g, 256, 0, s>>>(static_cast<const uint32_t*>(in), outer, n, out);
+    }
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k6_scan_inner");
+    return IH_OK;
+  }
+  const int64_t bx = (inner + 31) / 32;
+  if (bx > 0x7fffffffLL) return fail(IH_ERR_PARAM, "too many columns");
+  const dim3 grid((unsigned)bx, (unsigned)(outer < 65535 ? outer : 65535));
+  if (elem_bytes == 1)
+    ih::k6_scan_strided<uint8_t><<<grid, 1024, 0, s>>>(static_cast<const uint8_t*>(in), outer, n,
+                                                       inner, out);
+  else
+    ih::k6_scan_strided<uint32_t><<<grid, 1024, 0, s>>>(static_cast<const uint32_t*>(in), outer,
+                                                        n, inner, out);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k6_scan_strided");
+  return IH_OK;
+}
+
+ih_status ih_transpose(const void* in, int64_t rows, int64_t cols, int32_t elem_bytes, void* out,
+                       void* stream) {
+  if (rows < 0 || cols < 0) return fail(IH_ERR_PARAM, "extents must be >= 0");
+  if (rows == 0 || cols == 0) return IH_OK;
+  if (!in || !out) return fail(IH_ERR_PARAM, "null pointer");
+  const int64_t bx = (cols + 31) / 32, by = (rows + 31) / 32;
+  if (bx > 0x7fffffffLL) return fail(IH_ERR_PARAM, "too many columns");
+  const dim3 grid((unsigned)bx, (unsigned)(by < 65535 ? by : 65535));
+  cudaStream_t s = (cudaStream_t)stream;
+  switch (elem_bytes) {
+    case 1: ih::k6_transpose<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)in, rows, cols, (uint8_t*)out); break;
+    case 2: ih::k6_transpose<uint16_t><<<grid, 256, 0, s>>>((const uint16_t*)in, rows, cols, (uint16_t*)out); break;
+    case 4: ih::k6_transpose<uint32_t><<<grid, 256, 0, s>>>((const uint32_t*)in, rows, cols, (uint32_t*)out); break;
+    case 8: ih::k6_transpose<uint64_t><<<grid, 256, 0, s>>>((const uint64_t*)in, rows, cols, (uint64_t*)out); break;
+    case 16:
+      if (((uintptr_t)in | (uintptr_t)out) & 15) return fail(IH_ERR_PARAM, "16-byte elements need 16-byte alignment");
+      ih::k6_transpose<uint4><<<grid, 256, 0, s>>>((const uint4*)in, rows, cols, (uint4*)out);
+      break;
+    default: return fail(IH_ERR_PARAM, "elem_bytes must be 1, 2, 4, 8 or 16");
+  }
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k6_transpose");
+  return IH_OK;
+}
+
 void ih_debug_trace(void* device_buffer, size_t ctas) {
   g_trace = (unsigned long long*)device_buffer;
   g_trace_ctas = device_buffer ? ctas : 0;
@@ -941,6 +1035,6 @@ const char* ih_status_string(ih_status s) {
 
 const char* ih_last_error(void) { return g_last_error; }
 
-int32_t ih_abi_version(void) { return (1 << 16) | 3; }
+int32_t ih_abi_version(void) { return (1 << 16) | 4; }
 
 }  // extern "C"

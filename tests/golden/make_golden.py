@@ -17,6 +17,12 @@ Fixtures:
                          (synth_image seed 0; HD frames seeds 0..63), computed here
                          with the reference; the 8192x8192x256 per-plane values are
                          SURVEY.md Appendix A (reference compute_streamed, 698 s).
+  scans.npz           -- the reference scan module (scan.py:33-103) on edge
+                         inputs: 1-D scans across the device tile size, u64 wrap,
+                         negative ints, overflow at / past the last prefix,
+                         plane scans of several dtypes, transposes;
+                         ``<case>__raises`` holds the exception name, ``<case>__in_of``
+                         the case whose input it shares.
   small_cases.npz     -- full reference tensors for hand-picked edge cases
                          (known answers of tests/test_strategies.py, explicit LUTs,
                          B=256, ragged shapes), plus reference region_histogram
@@ -152,7 +158,70 @@ def small_cases():
     return cases
 
 
+def scans():
+    """Reference scan-module outputs (scan.py:33-103) on edge inputs."""
+    from inthist import scan as S
+
+    rng = np.random.default_rng(SEED + 200)
+    out, seen = {}, {}
+
+    def run(name, fn, x, *args):
+        if id(x) in seen:  # shared input: stored once, referenced by name
+            out[f"{name}__in_of"] = np.array(seen[id(x)])
+        else:
+            seen[id(x)] = name
+            out[f"{name}__in"] = np.asarray(x)
+        try:
+            out[f"{name}__out"] = np.asarray(fn(x, *args))
+        except Exception as exc:  # noqa: BLE001 - the class name is the fixture
+            out[f"{name}__raises"] = np.array(type(exc).__name__)
+
+    for n in (1, 2, 255, 2047, 2048, 2049, 4096 + 3, 10_007):
+        x = rng.integers(0, 1000, n).astype(np.uint16)
+        run(f"incl_{n}", S.inclusive_scan, x)
+        run(f"excl_{n}", S.exclusive_scan, x)
+        run(f"blk7_{n}", S.blocked_scan, x, 7)
+    big = np.full(5000, 2**20, dtype=np.int64)  # 2^20 * 4096 = 2^32: overflow at i = 4095
+    run("incl_over_mid", S.inclusive_scan, big)
+    run("excl_over_mid", S.exclusive_scan, big)
+    run("excl_last_only", S.exclusive_scan, np.array([2**32 - 1, 5], dtype=np.int64))
+    run("incl_last_only", S.inclusive_scan, np.array([2**32 - 1, 5], dtype=np.int64))
+    run("incl_neg_wrap", S.inclusive_scan, np.array([5, -3, 2], dtype=np.int64))
+    run("incl_neg_over", S.inclusive_scan, np.array([-1], dtype=np.int64))
+    run("incl_huge_elem", S.inclusive_scan, np.array([2**40], dtype=np.int64))
+    run("incl_u64_wrap", S.inclusive_scan, np.array([5, 2**64 - 5, 3], dtype=np.uint64))
+    run("incl_u64_over", S.inclusive_scan, np.array([2**63, 2**63, 7], dtype=np.uint64))
+    run("incl_int8", S.inclusive_scan, np.array([-1, 1, 100], dtype=np.int8))
+    run("incl_2d", S.inclusive_scan, rng.integers(0, 50, (13, 17)))
+    run("incl_bool", S.inclusive_scan, rng.random(3000) < 0.5)
+    for name, plane in (
+        ("u32", rng.integers(0, 2**32, (37, 53), dtype=np.uint64).astype(np.uint32)),
+        ("u8", rng.integers(0, 256, (65, 300), dtype=np.uint8)),
+        ("i64", rng.integers(-2**40, 2**40, (5, 1000), dtype=np.int64)),
+        ("bool", rng.random((17, 9)) < 0.3),
+        ("tall", rng.integers(0, 2**31, (3000, 3), dtype=np.uint64).astype(np.uint32)),
+        ("wide", rng.integers(0, 2**31, (2, 3000), dtype=np.uint64).astype(np.uint32)),
+        ("vec", rng.integers(0, 9, 40, dtype=np.uint32)),
+    ):
+        run(f"rows_{name}", S.scan_rows, plane)
+        run(f"cols_{name}", S.scan_cols, plane)
+    for name, plane in (
+        ("u8", rng.integers(0, 256, (33, 65), dtype=np.uint8)),
+        ("u16", rng.integers(0, 2**16, (70, 31), dtype=np.uint16)),
+        ("u32", rng.integers(0, 2**32, (100, 3), dtype=np.uint64).astype(np.uint32)),
+        ("f64", rng.random((45, 64))),
+        ("c128", rng.random((9, 40)) + 1j * rng.random((9, 40))),
+        ("one", np.array([[7]], dtype=np.uint32)),
+    ):
+        run(f"tr_{name}", S.transpose, plane)
+    return out
+
+
 def main():
+    if "--only-scans" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "scans.npz"), **scans())
+        return
+    np.savez_compressed(os.path.join(HERE, "scans.npz"), **scans())
     inst = c1_instances()
     with open(os.path.join(HERE, "c1_instances.json"), "w") as fh:
         json.dump(inst, fh, indent=0)
