@@ -510,7 +510,7 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
   if (env_int("IH_COLCOUNTS_SLAB", 0) == 0) {  // all bins in one pass (shared atomics)
     dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
     auto kern = al ? ih::k2_colcounts_all<true> : ih::k2_colcounts_all<false>;
-    const size_t smem = (size_t)p.nbp * 64 * sizeof(uint32_t);
+    const size_t smem = (size_t)(p.nbp + 1) * 64 * sizeof(uint32_t);
     if (!set_dyn_smem((const void*)kern, smem))
       return cuda_fail("k2_colcounts_all smem attribute");
     if (launch(kern, grid, dim3(256), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,

@@ -144,15 +144,28 @@ __global__ void __launch_bounds__(kCountWarps * 32) k2_colcounts(
 // (low half) and 4*lane+2h+1 (high half): increments are 1 << 16*(k&1), and
 // the bank is the lane, so a warp's atomics never conflict.  Counts per
 // segment are < 65536 (host-enforced), so halves never carry.  The dump is
-// directly the u16x4 layout of the table.
+// directly the u16x4 layout of the table.  Pixels outside the slab add into a
+// discard row, so the per-pixel add is unconditional (no branch), and rows
+// are addressed by stepping one pointer.  (Tried: counting 1- to 8-bin slabs
+// in registers through a one-hot u64 table -- 64-bit shared loads made it
+// 15-55 % slower than these shared adds; software-pipelining the row loads:
+// neutral.  The kernel is bound by the shared-memory pipe -- the LUT lookup
+// with ~3-way bank conflicts plus the add -- at ~6 pixels per clock per SM,
+// and runs mostly under the previous call's scan via PDL.)
 // ---------------------------------------------------------------------------
+// Shared-memory add without a return value, as PTX: atomicAdd(.., 1) would be
+// turned into warp-aggregated ATOMS.POPC.INC with a match loop per pixel.
+__device__ __forceinline__ void red_shared_add(uint32_t saddr, uint32_t v) {
+  asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
+}
+
 template <bool ALIGNED>
 __global__ void __launch_bounds__(256) k2_colcounts_all(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
     RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws,
     uint32_t* __restrict__ ctot) {
-  extern __shared__ __align__(16) uint32_t hist2[];  // [nbp][2][32]
-  __shared__ uint32_t sw[512];  // pixel (| 256 past the edge) -> word offset of its bin, or ~0
+  extern __shared__ __align__(16) uint32_t hist2[];  // [nbp + 1][2][32]: row nbp = discard
+  __shared__ uint32_t sw[512];  // pixel (| 256 past the edge) -> word offset of its bin row
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int nw = blockDim.x >> 5;
@@ -162,22 +175,22 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
   griddep_launch_dependents();
   for (int v = threadIdx.x; v < 512; v += blockDim.x) {
     const uint32_t b = v < 256 ? (uint32_t)lut.rel[v] : 0xffffffffu;
-    sw[v] = b < (uint32_t)nbp ? b * 64u : 0xffffffffu;
+    sw[v] = (b < (uint32_t)nbp ? b : (uint32_t)nbp) * 64u;  // outside the slab: discard row
   }
   {
     uint4* z = reinterpret_cast<uint4*>(hist2);
-    for (int i = threadIdx.x; i < nbp * 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < (nbp + 1) * 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
   uint32_t inval[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) inval[k] = (c + k < W) ? 0u : 256u;
   __syncthreads();
   uint32_t* hl = hist2 + lane;
+  const uint32_t hs = (uint32_t)__cvta_generic_to_shared(hl);
   const uint8_t* base = img + f * fstride;
   const int64_t seg0 = sg.start(s);
   const int64_t seg1 = min(sg.start(s + 1), H);
-  auto load_px = [&](int64_t r) -> uint32_t {
-    const uint8_t* row = base + r * pitch + c;
+  auto load_px = [&](const uint8_t* row) -> uint32_t {
     if (ALIGNED) return __ldg(reinterpret_cast<const uint32_t*>(row));
     uint32_t px = 0;
 #pragma unroll
@@ -188,18 +201,22 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
   auto count4 = [&](uint32_t px) {
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const uint32_t o = sw[((px >> (8 * k)) & 0xffu) | inval[k]];
-      if (o != 0xffffffffu) atomicAdd(hl + o + (k >> 1) * 32, 1u << (16 * (k & 1)));
+      const uint32_t v = ((px >> (8 * k)) & 0xffu) | inval[k];
+      red_shared_add(hs + 4 * (sw[v] + (k >> 1) * 32), 1u << (16 * (k & 1)));
     }
   };
   if (c < W) {
-    // rows seg0 + warp + i*nw; 8 rows of loads in flight per warp
+    // rows seg0 + warp + i*nw; 8 rows of loads in flight per warp, addressed
+    // by stepping one row pointer (no 64-bit multiply per load)
     constexpr int U = 8;
+    const int64_t rstep = (int64_t)nw * pitch;
     const int64_t step = (int64_t)nw * U;
-    for (int64_t r = seg0 + warp; r < seg1; r += step) {
+    const uint8_t* p = base + (seg0 + warp) * pitch + c;
+    for (int64_t r = seg0 + warp; r < seg1; r += step, p += U * rstep) {
       uint32_t px[U];
+      const uint8_t* q = p;
 #pragma unroll
-      for (int i = 0; i < U; ++i) px[i] = r + i * nw < seg1 ? load_px(r + i * nw) : 0u;
+      for (int i = 0; i < U; ++i, q += rstep) px[i] = r + i * nw < seg1 ? load_px(q) : 0u;
 #pragma unroll
       for (int i = 0; i < U; ++i)
         if (r + i * nw < seg1) count4(px[i]);
