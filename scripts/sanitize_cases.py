@@ -1,6 +1,7 @@
 """Small parity cases for compute-sanitizer: every K2 carry mode / input path,
 column tiles (k2_rowleft), both count-table kernels,
-K1/K1b, K3, K4, K5 -- each checked against the oracle."""
+K1/K1b, K3, K4, K5, and the K6 scan-module kernels -- each checked against
+the oracle / numpy."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np, torch
@@ -39,4 +40,25 @@ assert np.array_equal(device.window_counts(t, 7, 9).cpu().numpy(), O.window_coun
 tm = np.ones(6) / 6
 d = device.likelihood_map(t, tm, 7, 9, "intersection").cpu().numpy()
 assert np.abs(d - O.np_likelihood_map(t.cpu().numpy(), tm, 7, 9, "intersection")).max() < 1e-12
+# K6: 1-D scans (aligned / unaligned views, overflow flag), axis scans (u8 / u32,
+# vector and scalar rows, middle axis), transposes of every element size
+from paper_1711_01919_b200 import scan as S
+from paper_1711_01919_b200.errors import ScanOverflowError
+v = torch.from_numpy(rng.integers(0, 100, 5001)).cuda()
+for off in (0, 1):
+    got = S.inclusive_scan(v[off:]).cpu().numpy()
+    bad += not np.array_equal(got, np.cumsum(v[off:].cpu().numpy()).astype(np.uint32))
+    bad += int(S.exclusive_scan(v[off:]).cpu().numpy()[-1]) != int(got[-2])
+try:
+    S.inclusive_scan(np.array([2**32 - 1, 1]))
+    bad += 1
+except ScanOverflowError:
+    pass
+for shape, dt in (((33, 260), np.uint8), ((33, 259), np.uint8), ((17, 64), np.uint32), ((5, 3, 7), np.uint32)):
+    a = rng.integers(0, 200, shape).astype(dt)
+    for ax, fn in ((1, S.scan_rows), (0, S.scan_cols)):
+        bad += not np.array_equal(fn(a), np.cumsum(a, axis=ax, dtype=np.uint32))
+for dt in (np.uint8, np.uint16, np.uint32, np.float64, np.complex128):
+    a = (rng.random((37, 45)) * 100).astype(dt)
+    bad += not np.array_equal(S.transpose(a), a.T)
 print("sanitize cases done, mismatches:", bad)
