@@ -15,6 +15,9 @@
  *   ih_region_histograms    <- core.py:179-195 region_histogram (batched).
  *   ih_window_counts        <- likelihood.py:34-52 window_counts.
  *   ih_likelihood_map       <- likelihood.py:55-77 likelihood_map (fused).
+ *   ih_scan_u64             <- scan.py:33-76 inclusive/exclusive/blocked_scan.
+ *   ih_scan_axis_u32        <- scan.py:79-92 scan_rows / scan_cols.
+ *   ih_transpose            <- scan.py:95-103 transpose.
  *
  * Conventions (all entry points):
  *   - stream-ordered and asynchronous: work is enqueued on `stream`; nothing

@@ -130,3 +130,13 @@ def test_transpose_large_rows_grid():
     a = torch.randint(0, 2**15, (65536 * 32 + 17, 3), dtype=torch.int16, device="cuda")
     t = S.transpose(a)
     assert torch.equal(t, a.t().contiguous())
+
+
+def test_repeated_calls(rng):
+    """Back-to-back calls on one stream (the overflow flag and tile totals are
+    reset per call), sizes from one tile to many."""
+    for n in (1, 2047, 2048, 2049, 100_000, 3_000_001, 7):
+        x = torch.from_numpy(rng.integers(0, 1000, n)).cuda()
+        want = np.cumsum(x.cpu().numpy()).astype(np.uint32)
+        for _ in range(3):
+            assert np.array_equal(S.inclusive_scan(x).cpu().numpy(), want), n
