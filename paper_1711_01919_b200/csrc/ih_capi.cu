@@ -291,8 +291,11 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   // Each segment costs a u16 count slot of 1/(2S) of the output (mostly L2).
   const int64_t slots = (int64_t)kNumSMs * ctas_per_sm(p);
   const int64_t units = frames * p.ngroups * p.T;
-  // 32-row minimum segments; 16 for short images (512^2: 24.0 -> 19.4 us/call)
-  const int64_t min_rows = env_int("IH_MIN_SEG_ROWS", H >= 256 && H <= 768 ? 16 : 32);
+  // 32-row minimum segments; 16 for short images, 8 up to 512 rows (single
+  // 512^2 x 32 frame: 24.0 -> 18.7 -> 16.7 us/call graph-timed; 384^2 17.7 ->
+  // 13.9; 600 / 768 rows are faster at 16, profiles/r01i/min_segment_rows.txt)
+  const int64_t min_rows =
+      env_int("IH_MIN_SEG_ROWS", H >= 256 && H <= 512 ? 8 : H > 512 && H <= 768 ? 16 : 32);
   const int64_t max_seg = (H + min_rows - 1) / min_rows;
   const bool many = units * 4 >= slots;  // >= a quarter wave without segments
   double waves = many ? 4.0 : (p.big ? 8.0 : 2.0);

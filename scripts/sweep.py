@@ -47,6 +47,12 @@ WL = {
   "hdp64": (1600, 900, 32, 64, None),
   "qhd16": (2560, 1440, 32, 16, None),
   "uhd8": (3840, 2160, 32, 8, None),
+  "vga1": (640, 480, 32, 1, None),
+  "svga1": (800, 600, 32, 1, None),
+  "s384": (384, 384, 32, 1, None),
+  "s768": (768, 768, 32, 1, None),
+  "512b16": (512, 512, 16, 1, None),
+  "512b64": (512, 512, 64, 1, None),
 }
 def run(name, reps=5, kernel="auto"):
     W, H, B, F, br = WL[name]
