@@ -371,6 +371,51 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
 #pragma unroll
     for (int q = 0; q < P; ++q) acc[q] = 0.0;
     constexpr int U = P >= 4 ? 2 : 4;  // bins per step
+    if (i > 0 && j > 0 && j + P <= C) {
+      // interior placements (all but the first row / column and a ragged
+      // tail): no predicates, the four corner pointers and the table row step
+      // by one plane / one table row per bin -- the general path below spends
+      // most of its issue slots on 64-bit address arithmetic and predicates
+      const uint32_t* p11 = t + o11;
+      const uint32_t* p10 = t + o10;
+      const uint32_t* p01 = t + o01;
+      const uint32_t* p00 = t + o00;
+      const double* Mb = M;
+      int b = 0;
+      for (; b + U <= nb; b += U) {
+        uint32_t n[U][P];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int q = 0; q < P; ++q)
+            n[u][q] = __ldg(p11 + q) - __ldg(p10 + q) - __ldg(p01 + q) + __ldg(p00 + q);
+          p11 += plane, p10 += plane, p01 += plane, p00 += plane;
+        }
+        double m[U][P];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+#pragma unroll
+          for (int q = 0; q < P; ++q) m[u][q] = __ldg(Mb + n[u][q]);
+          Mb += n1;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)  // bin order b = 0..nb-1
+#pragma unroll
+          for (int q = 0; q < P; ++q) acc[q] += m[u][q];
+      }
+      for (; b < nb; ++b) {
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const uint32_t c = __ldg(p11 + q) - __ldg(p10 + q) - __ldg(p01 + q) + __ldg(p00 + q);
+          acc[q] += __ldg(Mb + c);
+        }
+        p11 += plane, p10 += plane, p01 += plane, p00 += plane;
+        Mb += n1;
+      }
+#pragma unroll
+      for (int q = 0; q < P; ++q) out[i * C + j + q] = fmin(fmax(acc[q], 0.0), 1.0);
+      continue;
+    }
     for (int b0 = 0; b0 < nb; b0 += U) {
       uint32_t n[U][P];
 #pragma unroll
