@@ -871,7 +871,7 @@ ih_status ih_likelihood_map_ws(const uint32_t* t, int32_t nb, int64_t height, in
       ih::k5_metric_table<false><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
           tpl, nb, (int64_t)h * w, M);
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k5_metric_table");
-    const int64_t P = env_int("IH_K5_PAIRS", 2);  // adjacent placements per thread
+    const int64_t P = env_int("IH_K5_PAIRS", 2);  // placements per thread (32 apart)
     if (P == 2 || P == 4) {
       dim3 grid((unsigned)((C + 256 * P - 1) / (256 * P)), (unsigned)(R < 65535 ? R : 65535));
       auto k = P == 4 ? ih::k5_likelihood_map_tabp<4> : ih::k5_likelihood_map_tabp<2>;

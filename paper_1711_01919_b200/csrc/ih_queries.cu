@@ -345,10 +345,10 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tab(const uint32_t* __r
   }
 }
 
-// K5 (table, P adjacent placements per thread): each bin's four corner
-// pointers serve P placements (loads at +0..+P-1): a P-th of the address
-// arithmetic per placement.  Same terms, same bin order: bit-identical to
-// k5_likelihood_map / _tab.
+// K5 (table, P placements per thread, 32 apart): each bin's four corner
+// pointers serve P placements (loads at +0, +32, ...): a P-th of the address
+// arithmetic per placement, and every warp load is one coalesced run.  Same
+// terms, same bin order: bit-identical to k5_likelihood_map / _tab.
 template <int P>
 __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __restrict__ t, int nb,
                                                                int64_t H, int64_t W, int h, int w,
@@ -358,7 +358,10 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
   const int64_t n1 = (int64_t)h * w + 1;
   const int64_t plane = H * W;
   for (int64_t i = blockIdx.y; i < R; i += gridDim.y) {
-    const int64_t j = P * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+    // a warp covers 32*P consecutive placements, lane l taking l, l+32, ...:
+    // every corner load and output store of the warp is one coalesced run
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t j = (g >> 5) * (32 * P) + (g & 31);
     if (j >= C) continue;
     const int64_t o11 = (i + h - 1) * W + (j + w - 1);
     const int64_t o01 = (i - 1) * W + (j + w - 1);
@@ -366,12 +369,12 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
     const int64_t o00 = (i - 1) * W + (j - 1);
     bool ok[P];
 #pragma unroll
-    for (int q = 0; q < P; ++q) ok[q] = j + q < C;
+    for (int q = 0; q < P; ++q) ok[q] = j + 32 * q < C;
     double acc[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) acc[q] = 0.0;
     constexpr int U = P >= 4 ? 2 : 4;  // bins per step
-    if (i > 0 && j > 0 && j + P <= C) {
+    if (i > 0 && j > 0 && j + 32 * (P - 1) < C) {
       // interior placements (all but the first row / column and a ragged
       // tail): no predicates, the four corner pointers and the table row step
       // by one plane / one table row per bin -- the general path below spends
@@ -388,7 +391,7 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
         for (int u = 0; u < U; ++u) {
 #pragma unroll
           for (int q = 0; q < P; ++q)
-            n[u][q] = __ldg(p11 + q) - __ldg(p10 + q) - __ldg(p01 + q) + __ldg(p00 + q);
+            n[u][q] = __ldg(p11 + 32 * q) - __ldg(p10 + 32 * q) - __ldg(p01 + 32 * q) + __ldg(p00 + 32 * q);
           p11 += plane, p10 += plane, p01 += plane, p00 += plane;
         }
         double m[U][P];
@@ -406,14 +409,14 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
       for (; b < nb; ++b) {
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-          const uint32_t c = __ldg(p11 + q) - __ldg(p10 + q) - __ldg(p01 + q) + __ldg(p00 + q);
+          const uint32_t c = __ldg(p11 + 32 * q) - __ldg(p10 + 32 * q) - __ldg(p01 + 32 * q) + __ldg(p00 + 32 * q);
           acc[q] += __ldg(Mb + c);
         }
         p11 += plane, p10 += plane, p01 += plane, p00 += plane;
         Mb += n1;
       }
 #pragma unroll
-      for (int q = 0; q < P; ++q) out[i * C + j + q] = fmin(fmax(acc[q], 0.0), 1.0);
+      for (int q = 0; q < P; ++q) out[i * C + j + 32 * q] = fmin(fmax(acc[q], 0.0), 1.0);
       continue;
     }
     for (int b0 = 0; b0 < nb; b0 += U) {
@@ -428,11 +431,11 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
         const uint32_t* p00 = p + o00;
 #pragma unroll
         for (int q = 0; q < P; ++q) {
-          const bool left = j + q > 0;
-          const uint32_t a11 = ok[q] ? __ldg(p11 + q) : 0u;
-          const uint32_t a10 = ok[q] && left ? __ldg(p10 + q) : 0u;
-          const uint32_t a01 = ok[q] && i > 0 ? __ldg(p01 + q) : 0u;
-          const uint32_t a00 = ok[q] && i > 0 && left ? __ldg(p00 + q) : 0u;
+          const bool left = j + 32 * q > 0;
+          const uint32_t a11 = ok[q] ? __ldg(p11 + 32 * q) : 0u;
+          const uint32_t a10 = ok[q] && left ? __ldg(p10 + 32 * q) : 0u;
+          const uint32_t a01 = ok[q] && i > 0 ? __ldg(p01 + 32 * q) : 0u;
+          const uint32_t a00 = ok[q] && i > 0 && left ? __ldg(p00 + 32 * q) : 0u;
           n[u][q] = a11 - a10 - a01 + a00;  // exact window count
         }
       }
@@ -453,7 +456,7 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
     }
 #pragma unroll
     for (int q = 0; q < P; ++q)
-      if (ok[q]) out[i * C + j + q] = fmin(fmax(acc[q], 0.0), 1.0);
+      if (ok[q]) out[i * C + j + 32 * q] = fmin(fmax(acc[q], 0.0), 1.0);
   }
 }
 
