@@ -874,7 +874,12 @@ ih_status ih_likelihood_map_ws(const uint32_t* t, int32_t nb, int64_t height, in
     const int64_t P = env_int("IH_K5_PAIRS", 2);  // placements per thread (32 apart)
     if (P == 2 || P == 4) {
       dim3 grid((unsigned)((C + 256 * P - 1) / (256 * P)), (unsigned)(R < 65535 ? R : 65535));
-      auto k = P == 4 ? ih::k5_likelihood_map_tabp<4> : ih::k5_likelihood_map_tabp<2>;
+      // bins per step (P = 2): 2 -> 48 registers, the best occupancy / MLP
+      // balance (HD x32 64x64: U 2 / 4 / 8 = 0.0996 / 0.108 / 0.101 ms)
+      const int64_t ub = env_int("IH_K5_U", 2);
+      auto k = P == 4 ? ih::k5_likelihood_map_tabp<4>
+             : ub == 8 ? ih::k5_likelihood_map_tabp<2, 8>
+             : ub == 2 ? ih::k5_likelihood_map_tabp<2, 2> : ih::k5_likelihood_map_tabp<2, 4>;
       k<<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h, w, M, out);
       if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k5_likelihood_map_tabp");
       return IH_OK;

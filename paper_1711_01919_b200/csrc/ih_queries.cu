@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tab(const uint32_t* __r
 // pointers serve P placements (loads at +0, +32, ...): a P-th of the address
 // arithmetic per placement, and every warp load is one coalesced run.  Same
 // terms, same bin order: bit-identical to k5_likelihood_map / _tab.
-template <int P>
+template <int P, int UB = (P >= 4 ? 2 : 4)>
 __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __restrict__ t, int nb,
                                                                int64_t H, int64_t W, int h, int w,
                                                                const double* __restrict__ M,
@@ -373,7 +373,7 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
     double acc[P];
 #pragma unroll
     for (int q = 0; q < P; ++q) acc[q] = 0.0;
-    constexpr int U = P >= 4 ? 2 : 4;  // bins per step
+    constexpr int U = UB;  // bins per step
     if (i > 0 && j > 0 && j + 32 * (P - 1) < C) {
       // interior placements (all but the first row / column and a ragged
       // tail): no predicates, the four corner pointers and the table row step
