@@ -2,8 +2,14 @@
 """Benchmark: integral histograms/s and output GB/s (% of HBM) on B200.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--workload hd64|4k128|8k256] [--gather]
+                    [--workload 512|hd64|4k128|8k256] [--gather] [--dry-run]
 
+`--gpus N` is authoritative: under torchrun WORLD_SIZE must equal N; run
+directly with N > 1, bench.py re-launches itself under torch.distributed.run
+with N ranks (and exits non-zero when fewer than N GPUs are visible).
+
+`512` is configs[1] (512x512x32, one image per step, a replica per GPU;
+CUDA-graph replayed steps, eager calls reported beside them).
 Default workload (BASELINE.json configs[2], the north-star's 70 % target
 config): 1920x1080 uint8 frames, 32 uniform bins, a batch of 64 frames per
 step, frame-sharded across the N ranks (strong scaling: 64 frames in total).
@@ -66,6 +72,9 @@ class Workload:
 
 
 WORKLOADS = {
+    "512": Workload("512", 512, 512, 32, 1, "replicas",
+                    "512x512 u8 image, 32 uniform bins, one image per step (BASELINE cfg1), "
+                    "one replica per GPU"),
     "hd64": Workload("hd64", 1920, 1080, 32, 64, "frames",
                      "1920x1080 u8 frames, 32 uniform bins, 64-frame batch (BASELINE cfg2), "
                      "frame-sharded"),
@@ -184,6 +193,19 @@ def cpu_sample(wl: Workload, budget_s: float = 20.0):
 
     cores = O.max_threads()
     lut = uniform_table(wl.bins)
+    if wl.shard == "replicas":  # one small image per step: repeat it within the budget
+        img = synth_image(wl.width, wl.height, 0)
+        t1 = time.perf_counter()
+        O.compute_crossweave(img, lut, wl.bins)
+        per = max(time.perf_counter() - t1, 1e-6)
+        n = int(max(1, min(10000, budget_s / per)))
+        t1 = time.perf_counter()
+        for _ in range(n):
+            O.compute_crossweave(img, lut, wl.bins)
+        dt = time.perf_counter() - t1
+        return n / dt, cores, (f"{n} repetitions of synth_image({wl.width}, {wl.height}, 0) "
+                               f"x {wl.bins} bins, C port of reference compute_crossweave "
+                               f"(strategies.py:129-150), {cores} threads")
     if wl.shard == "frames":
         # size the sample from one timed frame so it stays within the budget
         first = synth_image(wl.width, wl.height, 0)
@@ -212,10 +234,30 @@ def cpu_sample(wl: Workload, budget_s: float = 20.0):
 
 
 def config_block(wl: Workload, world: int):
+    kind = {"frames": "frame-shard", "bins": "bin-shard", "replicas": "replica"}[wl.shard]
+    l2 = (f"no flush: per-step output {wl.frames * wl.out_bytes / 1e9:.1f} GB >> 126 MB L2"
+          if wl.frames * wl.out_bytes > 126e6 else
+          f"no flush: steps rotate over {SMALL_BUFFERS} input/output buffer sets "
+          f"({SMALL_BUFFERS * (wl.alg_bytes) / 1e6:.0f} MB > 126 MB L2)")
     return {"workload": wl.desc, "key": wl.key, "width": wl.width, "height": wl.height,
-            "bins": wl.bins, "histograms_per_step": wl.frames,
-            "parallelism": f"{'frame' if wl.shard == 'frames' else 'bin'}-shard x{world}",
-            "l2": f"no flush: per-step output {wl.frames * wl.out_bytes / 1e9:.1f} GB >> 126 MB L2"}
+            "bins": wl.bins, "histograms_per_step": step_histograms(wl, world),
+            "parallelism": f"{kind} x{world}", "l2": l2, "host_cpu": cpu_model()}
+
+
+SMALL_BUFFERS = 8  # cfg1: buffer sets the steps rotate over (> L2 in total)
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip() + f" ({os.cpu_count()} threads)"
+    except OSError:
+        pass
+    import platform
+
+    return platform.processor() or "unknown"
 
 
 def run_reference(args, wl: Workload, rank, world):
@@ -239,6 +281,55 @@ def run_reference(args, wl: Workload, rank, world):
         "output_gbs": value * wl.out_bytes / 1e9,
     }
     print(json.dumps(line), flush=True)
+
+
+def rank_share(wl: Workload, rank: int, world: int):
+    """This rank's frames [f0, f1) x bins [b0, b1): contiguous frame runs
+    (frame-sharded), bin slabs (bin-sharded, reference streaming.py:81-82), or
+    the whole workload per rank (replicas)."""
+    from paper_1711_01919_b200 import sharding
+
+    if wl.shard == "frames":
+        f0, f1 = sharding.frame_shards(wl.frames, world)[rank]
+        return f0, f1, 0, wl.bins
+    if wl.shard == "bins":
+        b0, b1 = sharding.bin_slabs(wl.bins, world)[rank]
+        return 0, wl.frames, b0, b1
+    return 0, wl.frames, 0, wl.bins
+
+
+def step_histograms(wl: Workload, world: int) -> int:
+    """Integral histograms all ranks complete per step."""
+    return wl.frames * world if wl.shard == "replicas" else wl.frames
+
+
+def run_dry(args, wl: Workload, rank, world):
+    """--dry-run: the N-rank plumbing without device work.  Each rank takes its
+    share, 'runs' for a rank-dependent host delay, and the step time is the max
+    over ranks -- the same reduction run_ours applies to its CUDA-event times."""
+    import torch
+    import torch.distributed as dist
+
+    share = rank_share(wl, rank, world)
+    t0 = time.perf_counter()
+    time.sleep(0.01 * (rank + 1))
+    ms = 1000.0 * (time.perf_counter() - t0)
+    shares = [share]
+    rank_ms = [ms]
+    if world > 1:
+        shares = [None] * world
+        dist.all_gather_object(shares, share)
+        rank_ms = [None] * world
+        dist.all_gather_object(rank_ms, ms)
+        t = torch.tensor([ms], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "metric": METRIC, "value": None, "unit": UNIT,
+                          "n_gpus": world, "ms_per_step": ms, "rank_ms": rank_ms,
+                          "shares": [list(x) for x in shares],
+                          "histograms_per_step": step_histograms(wl, world),
+                          "config": config_block(wl, world)}), flush=True)
 
 
 # ------------------------------------------------------------------ GPU side
@@ -477,6 +568,165 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     print(json.dumps(line), flush=True)
 
 
+def run_small(args, wl: Workload, rank, world, local_rank):
+    """cfg1 (512x512x32): one image per step -- a 33.8 MB problem whose kernels
+    run for a few microseconds, so the step is launch-bound unless the launches
+    are pre-recorded.  Each rank (a replica) cycles over SMALL_BUFFERS
+    (input, output, workspace) sets, > L2 in total.  ``value`` replays the
+    steps from CUDA graphs (8 one-image calls per graph, every call still one
+    full integral histogram); ``eager`` is the same K steps as plain
+    device.integral_histogram calls (preallocated output and workspace)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1711_01919_b200 import device, pipeline
+
+    import paper_1711_01919_b200 as ih
+
+    dev_index = local_rank % torch.cuda.device_count()
+    torch.cuda.set_device(dev_index)
+    dev = torch.device("cuda", dev_index)
+    spec = ih.BinSpec.uniform(wl.bins)
+    lut = spec.table
+    nbuf = SMALL_BUFFERS
+    host = synth_image(wl.width, wl.height, 0)
+    imgs = [device.upload_image(host, dev) for _ in range(nbuf)]
+    outs = [device.empty_output(1, wl.bins, wl.height, wl.width, dev)[0] for _ in range(nbuf)]
+    nws = max(16, device.workspace_bytes(1, wl.height, wl.width, wl.bins))
+    wss = [torch.empty(nws, dtype=torch.uint8, device=dev) for _ in range(nbuf)]
+    plan = device.plan(1, wl.height, wl.width, wl.bins)
+    stream = torch.cuda.Stream(dev)
+
+    def reduce_max(vals):
+        if world == 1:
+            return list(vals)
+        on = dev if dist.get_backend() == "nccl" else "cpu"
+        t = torch.tensor(list(vals), dtype=torch.float64, device=on)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return t.tolist()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def call(k):
+        device.integral_histogram(imgs[k], lut, wl.bins, out=outs[k], workspace=wss[k],
+                                  stream=stream)
+
+    with torch.cuda.stream(stream):
+        for k in range(nbuf):  # warm: attributes, plan caches
+            call(k)
+    torch.cuda.synchronize(dev)
+
+    def capture(fn):
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        return g
+
+    g_all = capture(lambda: [call(k) for k in range(nbuf)])
+    g_one = [capture(lambda k=k: call(k)) for k in range(nbuf)]
+    g_scan = capture(lambda: [device.scan(imgs[k], lut, wl.bins, outs[k], workspace=wss[k],
+                                          stream=stream) for k in range(nbuf)])
+
+    def graph_steps(n):
+        with torch.cuda.stream(stream):
+            for _ in range(n // nbuf):
+                g_all.replay()
+            for k in range(n % nbuf):
+                g_one[k].replay()
+
+    def eager_steps(n):
+        for i in range(n):
+            call(i % nbuf)
+
+    def timed(fn, n):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        barrier()
+        e0.record(stream)
+        fn(n)
+        e1.record(stream)
+        barrier()
+        return e0.elapsed_time(e1)
+
+    graph_steps(max(args.warmup, nbuf))
+    eager_steps(max(args.warmup, nbuf))
+    barrier()
+    with ClockSampler(dev_index) as clocks:
+        total_ms = timed(graph_steps, args.steps)
+    eager_ms = timed(eager_steps, args.steps)
+    # the scan kernel alone, back to back inside one graph (nbuf launches per replay)
+    reps = max(1, args.steps // nbuf)
+
+    def scan_steps(n):
+        with torch.cuda.stream(stream):
+            for _ in range(n):
+                g_scan.replay()
+
+    scan_ms = timed(scan_steps, reps) / (reps * nbuf)
+    gold = golden()["512x512x32"]["crc"]
+    crc_ok = all(f"{zlib.crc32(o.cpu().numpy().tobytes()):08x}" == gold for o in outs[:2])
+
+    e2e = None
+    if args.e2e_steps > 0:
+        pipe = pipeline.FramePipeline(1, wl.height, wl.width, spec, chunk=1)
+        h_in = pipeline.pinned_empty((1, wl.height, wl.width), dtype=torch.uint8)
+        h_in.copy_(torch.from_numpy(host[None]))
+        h_out = pipeline.pinned_empty((1, wl.bins, wl.height, wl.width))
+        n_e2e = max(args.e2e_steps, 20)
+        for _ in range(3):
+            pipe.run(h_in, h_out)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(n_e2e):
+            pipe.run(h_in, h_out)
+        barrier()
+        e2e_s = reduce_max([time.perf_counter() - t0])[0]
+        crc_ok = crc_ok and f"{zlib.crc32(h_out.numpy().tobytes()):08x}" == gold
+        e2e = {"value": world * n_e2e / e2e_s, "unit": UNIT,
+               "h2d_bytes_per_step": int(pipe.h2d_bytes) * world,
+               "d2h_bytes_per_step": int(pipe.d2h_bytes) * world, "steps": n_e2e,
+               "timer": "host perf_counter around synchronized steps"}
+
+    total_ms, eager_ms, scan_ms, bad = reduce_max([total_ms, eager_ms, scan_ms,
+                                                   0.0 if crc_ok else 1.0])
+    if rank != 0:
+        return
+    per_step = total_ms / args.steps
+    value = world * args.steps / (total_ms / 1000.0)
+    peak, peak_src = measured_peaks()
+    alg = wl.alg_bytes
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+        "config": dict(config_block(wl, world), timing="CUDA-graph replay, 8 one-image calls "
+                       "per graph; eager: the same steps as plain API calls"),
+        "output_gbs": value * wl.out_bytes / 1e9,
+        "hbm_frac_step": alg / (per_step / 1e3) / 1e9 / peak,
+        "us_per_call_graph": 1000.0 * per_step,
+        "eager": {"value": world * args.steps / (eager_ms / 1000.0), "unit": UNIT,
+                  "us_per_call": 1000.0 * eager_ms / args.steps},
+        "roofline": {"bound": "hbm", "kernel": "k2_scan", "achieved": alg / (scan_ms / 1e3) / 1e9,
+                     "peak": peak, "peak_source": peak_src, "unit": "GB/s",
+                     "frac": alg / (scan_ms / 1e3) / 1e9 / peak, "traffic": None,
+                     "alg_bytes_per_launch": alg, "launch_ms": scan_ms,
+                     "launch_timer": "CUDA events around graphs of 8 back-to-back scan launches"},
+        "gpu_launches": plan["launches"] * args.steps,
+        "plan": plan,
+        "parity": "output crc32 == reference golden 53891c64" if not bad else "MISMATCH",
+        "clocks": clocks.summary(),
+    }
+    if e2e is not None:
+        line["e2e"] = e2e
+    if world == 1 and args.cpu_baseline:
+        v, cores, sample = cpu_sample(wl, budget_s=args.ref_budget)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
+                                "sample": sample}
+    print(json.dumps(line), flush=True)
+
+
 def run_e2e(args, wl, spec, host, nloc, brange, out, dev, barrier, reduce_max, world):
     """Host buffers in, host buffers out, through pipeline.FramePipeline."""
     import torch
@@ -536,6 +786,9 @@ def main():
                     help="run each step's prepass and scan back to back on one stream")
     ap.add_argument("--ref-budget", type=float, default=10.0,
                     help="seconds of CPU work per reference sample (bounded)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher / partition / max-over-ranks plumbing only (no GPU work; "
+                         "CPU tests of the N>1 path)")
     args = ap.parse_args()
     if args.warmup < 3:
         ap.error("--warmup must be >= 3")
@@ -543,30 +796,80 @@ def main():
     if args.frames:  # sizing experiments, e.g. the per-GPU share of an N-GPU run
         wl = Workload(wl.key, wl.width, wl.height, wl.bins, args.frames, wl.shard,
                       wl.desc + f" [frames overridden: {args.frames}]")
+    if args.gpus < 1:
+        ap.error("--gpus must be >= 1")
+    launched = "WORLD_SIZE" in os.environ
+    if not launched and args.gpus > 1 and args.impl == "ours":
+        # `--gpus N` without a launcher: start N ranks ourselves (the driver's
+        # torchrun form sets WORLD_SIZE and lands in the branch below)
+        sys.exit(self_launch(args))
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if launched and world != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; they must agree",
+              file=sys.stderr)
+        sys.exit(2)
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
         return
+    backend = os.environ.get("IH_BENCH_BACKEND", "nccl")  # gloo: 1-GPU / CPU path tests only
+    if not args.dry_run:
+        import torch
+
+        ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if ndev < 1 or (backend == "nccl" and ndev < world):
+            print(f"bench.py: {world} rank(s) need {world} CUDA device(s), {ndev} visible "
+                  f"(one process per GPU; no CPU fallback)", file=sys.stderr)
+            sys.exit(3)
     if world > 1:
         import torch
         import torch.distributed as dist
 
-        backend = os.environ.get("IH_BENCH_BACKEND", "nccl")  # gloo: 1-GPU path test only
-        dev_index = local_rank % torch.cuda.device_count()
-        torch.cuda.set_device(dev_index)
-        if backend == "nccl":
+        if backend == "nccl" and not args.dry_run:
+            dev_index = local_rank % torch.cuda.device_count()
+            torch.cuda.set_device(dev_index)
             dist.init_process_group("nccl", device_id=torch.device("cuda", dev_index))
         else:
-            dist.init_process_group(backend)
+            if not args.dry_run:
+                torch.cuda.set_device(local_rank % torch.cuda.device_count())
+            dist.init_process_group("gloo")
     try:
-        run_ours(args, wl, rank, world, local_rank)
+        if args.dry_run:
+            run_dry(args, wl, rank, world)
+        elif wl.key == "512":
+            run_small(args, wl, rank, world, local_rank)
+        else:
+            run_ours(args, wl, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist
 
             dist.destroy_process_group()
+
+
+def self_launch(args) -> int:
+    """Re-run this command under torch.distributed.run with --gpus ranks (one
+    process per GPU, rendezvous on 127.0.0.1); returns the launcher's exit code."""
+    import socket
+    import subprocess
+
+    if not args.dry_run and os.environ.get("IH_BENCH_BACKEND", "nccl") == "nccl":
+        import torch
+
+        ndev = torch.cuda.device_count() if torch.cuda.is_available() else 0
+        if ndev < args.gpus:
+            print(f"bench.py: --gpus {args.gpus} needs {args.gpus} CUDA devices, {ndev} visible",
+                  file=sys.stderr)
+            return 3
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd).returncode
 
 
 if __name__ == "__main__":

@@ -15,6 +15,8 @@
  *   ih_region_histograms    <- core.py:179-195 region_histogram (batched).
  *   ih_window_counts        <- likelihood.py:34-52 window_counts.
  *   ih_likelihood_map       <- likelihood.py:55-77 likelihood_map (fused).
+ *   ih_wavefront            <- strategies.py:172-216 compute_wavefront with a
+ *                              trace: the tiled wavefront as scheduled.
  *   ih_scan_u64             <- scan.py:33-76 inclusive/exclusive/blocked_scan.
  *   ih_scan_axis_u32        <- scan.py:79-92 scan_rows / scan_cols.
  *   ih_transpose            <- scan.py:95-103 transpose.
@@ -134,15 +136,17 @@ ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t sl
  *   out      device (Q, nb) uint64
  * IH_ERR_BOUNDS if any region is degenerate or outside the tensor is NOT
  * detectable without a sync: the caller validates (the Python layer does,
- * core.py:142/:158 order); the kernel clamps nothing and reads only in-range
- * corners for valid regions. */
+ * for host and device regions, core.py:142/:158 order).  The kernel never
+ * reads outside the tensor: a degenerate or out-of-range region yields a
+ * row of zeros. */
 ih_status ih_region_histograms(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
                                const int32_t *regions, int64_t q, uint64_t *out, void *stream);
 
 /* Every h x w window's counts (likelihood.py:34-52).
- *   out  device (nb, height-h+1, width-w+1) int64
+ *   out  device (nb, height-h+1, width-w+1) int64, 8-byte aligned (16-byte
+ *        aligned takes the paired 16-byte-store kernel; otherwise 8-byte stores)
  * IH_ERR_PARAM if h < 1 or w < 1; IH_ERR_BOUNDS if h > height or w > width
- * (likelihood.py:36-41 order). */
+ * (likelihood.py:36-41 order); IH_ERR_PARAM if out is not 8-byte aligned. */
 ih_status ih_window_counts(const uint32_t *t, int32_t nb, int64_t height, int64_t width,
                            int32_t h, int32_t w, int64_t *out, void *stream);
 
@@ -206,6 +210,23 @@ ih_status ih_transpose(const void *in, int64_t rows, int64_t cols, int32_t elem_
 /* Debug: when set, k2_scan writes {start ns, prologue-done ns, end ns, SM id}
  * (4 u64) per CTA into the device buffer (grids of at most `ctas` CTAs).
  * NULL turns it off.  Not for production use (adds a barrier per CTA). */
+/* The wavefront tiled scan (WF-TiS) as actually scheduled, with its event
+ * trace (replaces the compute body of compute_wavefront(..., trace=list),
+ * strategies.py:172-216; the throughput path is ih_integral_histogram).
+ * t x t tiles run in dependency order: tile (i, j) starts only after (i-1, j)
+ * and (i, j-1) have finished.  Output: the full (bins, height, width) tensor,
+ * bit-identical to ih_integral_histogram, and
+ *   events   device, (ceil(H/t) * ceil(W/t), 2) uint32: per tile (row-major
+ *            tile index i*nj + j) the global sequence numbers of its "start"
+ *            and "finish" events (0, 1, 2, ... in the order they happened).
+ * workspace: >= ih_wavefront_workspace_bytes(height, width, tile) bytes.
+ * Errors: IH_ERR_PARAM for tile < 1 (first, strategies.py:185-186), then as
+ * ih_integral_histogram with frames = 1 and the full bin range. */
+size_t ih_wavefront_workspace_bytes(int64_t height, int64_t width, int32_t tile);
+ih_status ih_wavefront(const uint8_t *img, int64_t height, int64_t width, int64_t img_pitch,
+                       const uint8_t *lut256, int32_t bins, int32_t tile, uint32_t *out,
+                       uint32_t *events, void *workspace, size_t workspace_bytes, void *stream);
+
 void ih_debug_trace(void *device_buffer, size_t ctas);
 
 /* Human-readable status name. */

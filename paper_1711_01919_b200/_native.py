@@ -45,6 +45,8 @@ EXPORTS = (
     "ih_scan_u64",
     "ih_scan_axis_u32",
     "ih_transpose",
+    "ih_wavefront_workspace_bytes",
+    "ih_wavefront",
     "ih_status_string",
     "ih_last_error",
     "ih_abi_version",
@@ -101,6 +103,10 @@ def lib() -> ctypes.CDLL:
     L.ih_plan_describe.restype = ctypes.c_int
     L.ih_plan_hint.argtypes = [i64, i64, i64, i32, i32, i32, i32, i32]
     L.ih_plan_hint.restype = ctypes.c_int
+    L.ih_wavefront_workspace_bytes.argtypes = [i64, i64, i32]
+    L.ih_wavefront_workspace_bytes.restype = sz
+    L.ih_wavefront.argtypes = [P, i64, i64, i64, P, i32, i32, P, P, P, sz, P]
+    L.ih_wavefront.restype = ctypes.c_int
     L.ih_status_string.argtypes = [ctypes.c_int]
     L.ih_status_string.restype = ctypes.c_char_p
     L.ih_last_error.argtypes = []

@@ -18,7 +18,8 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 SRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libinthist_b200.so")
-SOURCES = ["ih_capi.cu", "ih_single_pass.cu", "ih_queries.cu", "ih_scan.cu", "ih_kernels.cuh"]
+SOURCES = ["ih_capi.cu", "ih_single_pass.cu", "ih_queries.cu", "ih_scan.cu", "ih_wavefront.cu",
+           "ih_kernels.cuh"]
 HEADER = os.path.join(ROOT, "include", "inthist_b200.h")
 
 NVCC_FLAGS = [

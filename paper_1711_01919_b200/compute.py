@@ -108,34 +108,36 @@ def compute_sts(img: GrayImage, spec: BinSpec, workers: int = 0) -> IntegralHist
     return _on_device(img, spec, _KERNEL_OF["sts"])
 
 
-def _tile_schedule(ni: int, nj: int):
-    """Anti-diagonal order of the reference's wavefront (strategies.py:210-215)."""
-    for d in range(ni + nj - 1):
-        yield [(i, d - i) for i in range(max(0, d - nj + 1), min(ni - 1, d) + 1)]
-
-
 def compute_wavefront(img: GrayImage, spec: BinSpec, tile: int = DEFAULT_TILE,
                       workers: int = 0, trace: list | None = None) -> IntegralHistogram:
     """WF-TiS entry point (strategies.py:172-216): tile, capacity, workers checks
-    in the reference's order, then K2.
+    in the reference's order, then the device pass.
 
-    ``trace`` is honoured at the level of the *logical* t x t tile schedule:
-    the device pass has no per-tile events (its carries replace the
-    wavefront), so the list receives, per anti-diagonal, "start" events for
-    every tile on it followed by "finish" events -- the dependency order the
-    K2 carries guarantee.  See DESIGN.md "wavefront trace".
+    Without ``trace`` the tensor comes from K2 (the single pass: its row-segment
+    carries replace the wavefront, and it is 10-100x faster).  With ``trace``
+    the wavefront itself runs on the device (K7, ih_wavefront): t x t tiles
+    claimed in anti-diagonal order, each starting only once the tiles above
+    and to the left have finished, and ``trace`` receives the recorded
+    ("start"|"finish", i, j) events in the order they happened (device-wide
+    sequence numbers, the analog of the reference's lock, :194-208).
     """
     if tile < 1:
         raise ParameterError(f"tile must be >= 1, got {tile}")
     img.check_capacity()
     resolve_workers(workers)
-    ih = _on_device(img, spec, _KERNEL_OF["wavefront"])
-    if trace is not None:
-        ni, nj = -(-img.height // tile), -(-img.width // tile)
-        for diag in _tile_schedule(ni, nj):
-            trace.extend(("start", i, j) for i, j in diag)
-            trace.extend(("finish", i, j) for i, j in diag)
-    return ih
+    if trace is None:
+        return _on_device(img, spec, _KERNEL_OF["wavefront"])
+    counts, ev = device.wavefront(device.upload_image(img.pixels), spec.table, spec.bins, tile)
+    nj = -(-img.width // tile)
+    seqs = ev.cpu().numpy()
+    events = []
+    for k, (s0, s1) in enumerate(seqs):
+        i, j = divmod(k, nj)
+        events.append((int(s0), "start", i, j))
+        events.append((int(s1), "finish", i, j))
+    events.sort()
+    trace.extend((kind, i, j) for _, kind, i, j in events)
+    return IntegralHistogram(device_counts=counts)
 
 
 def compute(img: GrayImage, spec: BinSpec, strategy: Strategy, workers: int = 0,

@@ -15,6 +15,7 @@
 #include "ih_queries.cu"
 #include "ih_scan.cu"
 #include "ih_single_pass.cu"
+#include "ih_wavefront.cu"
 
 namespace {
 
@@ -738,7 +739,11 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   // IH_K4_MODE 3 (default): pairs of adjacent outputs per 16-byte store;
   // 1: 4 strided outputs per thread; 0: the two-output kernel; 2: staged row
   // differences (while CW + w u32 fit in shared memory)
-  const int64_t k4mode = env_int("IH_K4_MODE", 3);
+  // mode 3's 16-byte pair stores need a 16-byte aligned `out`; int64 views
+  // at odd element offsets take the 8-byte-store kernel (mode 1)
+  int64_t k4mode = env_int("IH_K4_MODE", 3);
+  if (k4mode == 3 && ((uintptr_t)out & 15)) k4mode = 1;
+  if ((uintptr_t)out & 7) return fail(IH_ERR_PARAM, "out must be 8-byte aligned");
   if (k4mode == 3) {  // two adjacent outputs per 16-byte store
     const int U = env_int("IH_K4_PAIRS_U", 2) == 4 ? 4 : env_int("IH_K4_PAIRS_U", 2) == 1 ? 1 : 2;
     const int64_t cb = (C + 1 + 2 * 256 * U - 1) / (2 * 256 * U);  // U pairs per thread
@@ -1024,6 +1029,47 @@ ih_status ih_transpose(const void* in, int64_t rows, int64_t cols, int32_t elem_
   return IH_OK;
 }
 
+size_t ih_wavefront_workspace_bytes(int64_t height, int64_t width, int32_t tile) {
+  if (height < 1 || width < 1 || tile < 1) return 0;
+  const int64_t ntiles = ((height + tile - 1) / tile) * ((width + tile - 1) / tile);
+  return 16 + (size_t)(ntiles * 4 + 15) / 16 * 16;
+}
+
+ih_status ih_wavefront(const uint8_t* img, int64_t height, int64_t width, int64_t img_pitch,
+                       const uint8_t* lut256, int32_t bins, int32_t tile, uint32_t* out,
+                       uint32_t* events, void* workspace, size_t workspace_bytes, void* stream) {
+  if (tile < 1) return fail(IH_ERR_PARAM, "tile must be >= 1");  // strategies.py:185-186
+  Call c;
+  ih_status st = validate(img, 1, height, width, img_pitch, height * img_pitch, lut256, bins, 0,
+                          bins, IH_KERNEL_AUTO, &c);
+  if (st != IH_OK) return st;
+  if (!out || !events) return fail(IH_ERR_PARAM, "null pointer");
+  const int64_t ni = (height + tile - 1) / tile, nj = (width + tile - 1) / tile;
+  if (ni * nj > 0x7fffffffLL) return fail(IH_ERR_PARAM, "too many tiles");
+  const size_t need = ih_wavefront_workspace_bytes(height, width, tile);
+  if (!workspace || workspace_bytes < need)
+    return fail(IH_ERR_PARAM, "workspace too small (see ih_wavefront_workspace_bytes)");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(workspace, 0, need, s) != cudaSuccess) return cuda_fail("wavefront reset");
+  ih::WfArgs a;
+  a.img = img;
+  a.H = height;
+  a.W = width;
+  a.pitch = img_pitch;
+  a.nb = bins;
+  a.tile = tile;
+  a.ni = ni;
+  a.nj = nj;
+  a.ticket = (uint32_t*)workspace;
+  a.seq = a.ticket + 1;
+  a.flags = (uint32_t*)((uint8_t*)workspace + 16);
+  a.ev = events;
+  a.out = out;
+  ih::k7_wavefront<<<(unsigned)(ni * nj), ih::kWfWarps * 32, 0, s>>>(a, c.lut);
+  if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k7_wavefront");
+  return IH_OK;
+}
+
 void ih_debug_trace(void* device_buffer, size_t ctas) {
   g_trace = (unsigned long long*)device_buffer;
   g_trace_ctas = device_buffer ? ctas : 0;
@@ -1043,6 +1089,6 @@ const char* ih_status_string(ih_status s) {
 
 const char* ih_last_error(void) { return g_last_error; }
 
-int32_t ih_abi_version(void) { return (1 << 16) | 4; }
+int32_t ih_abi_version(void) { return (1 << 16) | 5; }
 
 }  // extern "C"

@@ -35,12 +35,18 @@ __global__ void __launch_bounds__(256) k3_region_histograms(const uint32_t* __re
        q += warps) {
     const int4 rg = __ldg(regions + q);  // r0, c0, r1, c1 (inclusive), warp-uniform
     const int64_t r0 = rg.x, c0 = rg.y, r1 = rg.z, c1 = rg.w;
+    unsigned long long* orow = out + q * nb;
+    if (r0 < 0 || c0 < 0 || r0 > r1 || c0 > c1 || r1 >= H || c1 >= W) {
+      // invalid region (the Python layer raises BoundsError before launch;
+      // a C caller gets zeros, never an out-of-bounds read)
+      for (int b = lane; b < nb; b += 32) orow[b] = 0ull;
+      continue;
+    }
     const bool top = r0 > 0, left = c0 > 0;
     const int64_t o11 = r1 * W + c1;
     const int64_t o01 = top ? (r0 - 1) * W + c1 : 0;
     const int64_t o10 = left ? r1 * W + (c0 - 1) : 0;
     const int64_t o00 = top && left ? (r0 - 1) * W + (c0 - 1) : 0;
-    unsigned long long* orow = out + q * nb;
     for (int b0 = 0; b0 < nb; b0 += 128) {
       uint32_t v[4][4];
 #pragma unroll

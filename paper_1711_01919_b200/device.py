@@ -409,6 +409,33 @@ def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None,
     return out
 
 
+def wavefront(image: torch.Tensor, table, bins: int, tile: int, stream=None):
+    """The wavefront tiled scan as scheduled on the device (K7, ih_wavefront).
+
+    ``image``: (H, W) uint8 CUDA tensor.  Returns ``(counts, events)``:
+    counts (bins, H, W) uint32 (bit-identical to integral_histogram) and
+    events, an (ni*nj, 2) int64 CUDA tensor holding for tile i*nj + j the
+    global sequence numbers of its "start" and "finish" (strategies.py:194-208).
+    """
+    if tile < 1:
+        raise ParameterError(f"tile must be >= 1, got {tile}")
+    a = _prepare_args(image, table, bins, None, "auto", stream)
+    if a.frames != 1:
+        raise ShapeError("wavefront takes one (H, W) image")
+    ni, nj = -(-a.H // tile), -(-a.W // tile)
+    out = empty_output(1, a.bins, a.H, a.W, a.dev)[0]
+    L = _native.lib()
+    need = int(L.ih_wavefront_workspace_bytes(a.H, a.W, int(tile)))
+    ctx = torch.cuda.stream(stream) if stream is not None else torch.cuda.device(a.dev)
+    with ctx:
+        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=a.dev)
+        ev = torch.empty((ni * nj, 2), dtype=torch.int32, device=a.dev)
+        _native.check(L.ih_wavefront(a.images.data_ptr(), a.H, a.W, a.pitch, a.lut.ctypes.data,
+                                     a.bins, int(tile), out.data_ptr(), ev.data_ptr(),
+                                     ws.data_ptr(), need, a.stream))
+    return out, ev.to(torch.int64)
+
+
 def _check_tensor(t: torch.Tensor) -> torch.Tensor:
     if t.dim() != 3 or t.dtype not in (torch.uint32, torch.int32):
         raise ShapeError("tensor must be a 3D uint32 array (bins, height, width)")
@@ -417,35 +444,65 @@ def _check_tensor(t: torch.Tensor) -> torch.Tensor:
     return t.contiguous()
 
 
-def region_histograms(t: torch.Tensor, regions, stream=None, out=None) -> torch.Tensor:
+_I32_MAX = (1 << 31) - 1
+
+
+def _validate_device_regions(regs: torch.Tensor, H: int, W: int) -> None:
+    """core.py:142 (degenerate) then core.py:158 (outside) for regions already
+    on the device: one fused reduction, one small D2H (a sync)."""
+    r0, c0, r1, c1 = regs.unbind(1)
+    bad = torch.stack([((r0 < 0) | (c0 < 0) | (r0 > r1) | (c0 > c1)).any(),
+                       ((r1 >= H) | (c1 >= W)).any(),
+                       (regs > _I32_MAX).any()]).cpu().tolist()
+    if bad[0]:
+        raise BoundsError("degenerate region")
+    if bad[1]:
+        raise BoundsError(f"region outside {W}x{H} image")
+    if bad[2]:
+        raise ParameterError("region coordinates must fit in int32")
+
+
+def region_histograms(t: torch.Tensor, regions, stream=None, out=None,
+                      validate: bool = True) -> torch.Tensor:
     """Batched core.py:179-195: (Q, 4) inclusive (r0,c0,r1,c1) -> (Q, nb) uint64.
 
-    Validation follows core.py:142 (degenerate) then core.py:158 (outside),
-    done on the host before launch when ``regions`` is host data.
+    Validation follows core.py:142 (degenerate) then core.py:158 (outside)
+    for host and device regions alike (device regions: one reduction and a
+    sync; ``validate=False`` skips it for regions the caller has already
+    checked -- the kernel never reads outside the tensor either way, but an
+    out-of-range region then yields unspecified counts).  Uploads and the
+    output allocation are ordered on ``stream`` (default: the current stream).
     """
     t = _check_tensor(t)
     nb, H, W = (int(x) for x in t.shape)
-    if isinstance(regions, torch.Tensor) and regions.is_cuda:
-        regs = regions.to(torch.int32).contiguous().view(-1, 4)
-    else:
-        r = np.ascontiguousarray(np.asarray(regions, dtype=np.int64).reshape(-1, 4))
-        if r.size:
-            if ((r[:, 0] < 0) | (r[:, 1] < 0) | (r[:, 0] > r[:, 2]) | (r[:, 1] > r[:, 3])).any():
-                raise BoundsError("degenerate region")
-            if ((r[:, 2] >= H) | (r[:, 3] >= W)).any():
-                raise BoundsError(f"region outside {W}x{H} image")
-        regs = torch.from_numpy(r.astype(np.int32)).to(t.device)
-    Q = int(regs.shape[0])
-    if out is None:
-        out = torch.empty((Q, nb), dtype=torch.uint64, device=t.device)
-    elif out.shape != (Q, nb) or out.dtype not in (torch.uint64, torch.int64) or \
-            not out.is_contiguous() or out.device != t.device:
-        raise ShapeError(f"out must be a contiguous ({Q}, {nb}) uint64 tensor on {t.device}")
-    if Q:
-        with torch.cuda.device(t.device):
+    st = stream if stream is not None else torch.cuda.current_stream(t.device)
+    with torch.cuda.device(t.device), torch.cuda.stream(st):
+        if isinstance(regions, torch.Tensor) and regions.is_cuda:
+            if regions.dtype.is_floating_point or regions.dtype == torch.bool:
+                raise ParameterError("regions must be an integer tensor")
+            r64 = regions.reshape(-1, 4).to(torch.int64)
+            if validate and r64.shape[0]:
+                _validate_device_regions(r64, H, W)
+            regs = r64.to(torch.int32).contiguous()
+        else:
+            r = np.ascontiguousarray(np.asarray(regions, dtype=np.int64).reshape(-1, 4))
+            if r.size:
+                if ((r[:, 0] < 0) | (r[:, 1] < 0) | (r[:, 0] > r[:, 2]) | (r[:, 1] > r[:, 3])).any():
+                    raise BoundsError("degenerate region")
+                if ((r[:, 2] >= H) | (r[:, 3] >= W)).any():
+                    raise BoundsError(f"region outside {W}x{H} image")
+                if (r > _I32_MAX).any():
+                    raise ParameterError("region coordinates must fit in int32")
+            regs = torch.from_numpy(r.astype(np.int32)).to(t.device, non_blocking=False)
+        Q = int(regs.shape[0])
+        if out is None:
+            out = torch.empty((Q, nb), dtype=torch.uint64, device=t.device)
+        elif out.shape != (Q, nb) or out.dtype not in (torch.uint64, torch.int64) or \
+                not out.is_contiguous() or out.device != t.device:
+            raise ShapeError(f"out must be a contiguous ({Q}, {nb}) uint64 tensor on {t.device}")
+        if Q:
             _native.check(_native.lib().ih_region_histograms(
-                t.data_ptr(), nb, H, W, regs.data_ptr(), Q, out.data_ptr(),
-                _stream_handle(t.device, stream)))
+                t.data_ptr(), nb, H, W, regs.data_ptr(), Q, out.data_ptr(), int(st.cuda_stream)))
     return out
 
 
@@ -464,12 +521,12 @@ def window_counts(t: torch.Tensor, h: int, w: int, stream=None, out=None) -> tor
     if h > H or w > W:
         raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
     shape = (nb, H - h + 1, W - w + 1)
-    out = torch.empty(shape, dtype=torch.int64, device=t.device) if out is None else \
-        _check_out(out, shape, (torch.int64,), t.device)
-    with torch.cuda.device(t.device):
+    st = stream if stream is not None else torch.cuda.current_stream(t.device)
+    with torch.cuda.device(t.device), torch.cuda.stream(st):
+        out = torch.empty(shape, dtype=torch.int64, device=t.device) if out is None else \
+            _check_out(out, shape, (torch.int64,), t.device)
         _native.check(_native.lib().ih_window_counts(
-            t.data_ptr(), nb, H, W, int(h), int(w), out.data_ptr(),
-            _stream_handle(t.device, stream)))
+            t.data_ptr(), nb, H, W, int(h), int(w), out.data_ptr(), int(st.cuda_stream)))
     return out
 
 

@@ -121,6 +121,17 @@ def deserialize_ih(data: bytes) -> IntegralHistogram:
     return IntegralHistogram(planes.astype(np.uint32).reshape(bins, height, width))
 
 
+def _pwrite_all(fd: int, buf: memoryview, offset: int) -> None:
+    """pwrite until every byte is written: one Linux write moves at most
+    0x7ffff000 bytes, so a multi-GB plane needs several calls."""
+    done, n = 0, len(buf)
+    while done < n:
+        k = os.pwrite(fd, buf[done:], offset + done)
+        if k <= 0:
+            raise OSError(f"pwrite wrote {k} bytes at offset {offset + done}")
+        done += k
+
+
 class TensorFileSink:
     """TensorSink writing (bin range, row range) pieces at their final offsets
     of an IHST file; thread-safe, usable with ``compute_streamed``."""
@@ -141,7 +152,7 @@ class TensorFileSink:
         with self._lock:
             for k, b in enumerate(range(bin_start, bin_stop)):
                 rows = np.ascontiguousarray(blocks[k]).astype("<u4", copy=False)
-                os.pwrite(self._fd, rows.tobytes(), self._offset(b, row_start))
+                _pwrite_all(self._fd, memoryview(rows).cast("B"), self._offset(b, row_start))
 
     def close(self):
         """Close the file (reference imgio.py:141-142)."""

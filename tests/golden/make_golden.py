@@ -23,6 +23,11 @@ Fixtures:
                          plane scans of several dtypes, transposes;
                          ``<case>__raises`` holds the exception name, ``<case>__in_of``
                          the case whose input it shares.
+  likelihood.npz      -- reference likelihood_map / best_match (likelihood.py:55-86)
+                         on random and structured images: both metrics, square,
+                         rectangular, 1x1 and full-image windows, B in {1, 3, 16,
+                         64, 256}, templates from normalize(region_histogram(...))
+                         (the reference tests' construction) and random ones.
   small_cases.npz     -- full reference tensors for hand-picked edge cases
                          (known answers of tests/test_strategies.py, explicit LUTs,
                          B=256, ragged shapes), plus reference region_histogram
@@ -217,11 +222,69 @@ def scans():
     return out
 
 
+def likelihood():
+    """Reference likelihood_map / best_match outputs (likelihood.py:55-86)."""
+    from inthist.likelihood import best_match, likelihood_map
+
+    rng = np.random.default_rng(SEED + 300)
+    out = {}
+
+    def add(name, px, spec, template, h, w, metric):
+        ih = inthist.compute_sequential(inthist.GrayImage(px), spec)
+        lm = likelihood_map(ih, template, h, w, metric)
+        r, c, v = best_match(lm)
+        out[f"{name}__img"] = px
+        out[f"{name}__lut"] = np.asarray(spec.table, dtype=np.uint8)
+        out[f"{name}__bins"] = np.array(spec.bins)
+        out[f"{name}__template"] = np.asarray(template, dtype=np.float64)
+        out[f"{name}__hw"] = np.array([h, w])
+        out[f"{name}__metric"] = np.array(metric)
+        out[f"{name}__map"] = lm.values
+        out[f"{name}__best"] = np.array([r, c], dtype=np.int64)
+        out[f"{name}__best_value"] = np.array(v)
+
+    def region_template(px, spec, reg):
+        ih = inthist.compute_sequential(inthist.GrayImage(px), spec)
+        return inthist.normalize(inthist.region_histogram(ih, inthist.Region(*reg)))
+
+    for metric in ("intersection", "bhattacharyya"):
+        m = metric[:5]
+        px = rng.integers(0, 256, (30, 40), dtype=np.uint8)
+        spec = inthist.BinSpec.uniform(16)
+        add(f"rnd40x30_b16_{m}", px, spec, region_template(px, spec, (10, 12, 17, 19)), 8, 8, metric)
+        px = rng.integers(0, 256, (61, 97), dtype=np.uint8)
+        spec = inthist.BinSpec.uniform(64)
+        add(f"rect97x61_b64_{m}", px, spec, region_template(px, spec, (3, 5, 22, 13)), 20, 9, metric)
+        spec = inthist.BinSpec.uniform(256)
+        px = rng.integers(0, 256, (64, 70), dtype=np.uint8)
+        add(f"b256_{m}", px, spec, region_template(px, spec, (0, 0, 15, 15)), 16, 16, metric)
+        tpl = rng.random(3)
+        tpl /= tpl.sum()
+        px = rng.integers(0, 256, (25, 33), dtype=np.uint8)
+        add(f"randtpl_b3_{m}", px, inthist.BinSpec.uniform(3), tpl, 5, 7, metric)
+        add(f"win1x1_b3_{m}", px, inthist.BinSpec.uniform(3), tpl, 1, 1, metric)
+        add(f"full_b3_{m}", px, inthist.BinSpec.uniform(3), tpl, 25, 33, metric)
+        add(f"b1_{m}", px, inthist.BinSpec.uniform(1), np.array([1.0]), 4, 4, metric)
+        # structured: blocks of constant value, so many windows tie (best_match tie rule)
+        blk = np.kron(rng.integers(0, 4, (6, 8)), np.ones((8, 8), dtype=np.int64)).astype(np.uint8) * 60
+        spec = inthist.BinSpec.uniform(8)
+        add(f"blocks64x48_b8_{m}", blk, spec, region_template(blk, spec, (8, 8, 15, 15)), 8, 8, metric)
+        tab = rng.integers(0, 5, 256)
+        px = rng.integers(0, 256, (40, 50), dtype=np.uint8)
+        spec = inthist.BinSpec.explicit(tab)
+        add(f"explicit5_{m}", px, spec, region_template(px, spec, (0, 0, 39, 49)), 12, 10, metric)
+    return out
+
+
 def main():
+    if "--only-likelihood" in sys.argv:
+        np.savez_compressed(os.path.join(HERE, "likelihood.npz"), **likelihood())
+        return
     if "--only-scans" in sys.argv:
         np.savez_compressed(os.path.join(HERE, "scans.npz"), **scans())
         return
     np.savez_compressed(os.path.join(HERE, "scans.npz"), **scans())
+    np.savez_compressed(os.path.join(HERE, "likelihood.npz"), **likelihood())
     inst = c1_instances()
     with open(os.path.join(HERE, "c1_instances.json"), "w") as fh:
         json.dump(inst, fh, indent=0)

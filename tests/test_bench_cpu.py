@@ -35,6 +35,60 @@ def test_reference_arm_json_line():
 
 
 def test_reference_arm_other_ranks_are_silent():
-    r = _run({"RANK": "1", "WORLD_SIZE": "2"})
+    r = _run({"RANK": "1", "WORLD_SIZE": "2"}, "--gpus", "2")
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+def _bench(*args, env=None):
+    e = dict(os.environ, **(env or {}))
+    e.pop("WORLD_SIZE", None)
+    return subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *args],
+                          capture_output=True, text=True, env=e, timeout=300)
+
+
+def test_gpus_flag_self_launches_ranks():
+    """`bench.py --gpus 2` (no launcher) starts 2 ranks under torch.distributed.run;
+    rank 0 reports n_gpus 2, the frame shards [0,32)/[32,64) and the step time as
+    the max over ranks (dry run: the plumbing without device work)."""
+    r = _bench("--gpus", "2", "--dry-run", "--steps", "3", "--warmup", "3")
+    assert r.returncode == 0, r.stderr
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2
+    assert d["shares"] == [[0, 32, 0, 32], [32, 64, 0, 32]]
+    assert d["ms_per_step"] == max(d["rank_ms"]) and d["rank_ms"][1] > d["rank_ms"][0]
+    assert d["config"]["parallelism"] == "frame-shard x2"
+
+
+def test_gpus_flag_bin_shards():
+    r = _bench("--gpus", "2", "--dry-run", "--workload", "4k128", "--steps", "3", "--warmup", "3")
+    assert r.returncode == 0, r.stderr
+    d = json.loads([l for l in r.stdout.splitlines() if l.startswith("{")][0])
+    assert d["shares"] == [[0, 1, 0, 64], [0, 1, 64, 128]]
+
+
+def test_gpus_flag_fails_loudly_without_devices():
+    """More ranks than visible GPUs: a clear error and a non-zero exit, never a
+    silent N=1 run."""
+    r = _bench("--gpus", "2", "--steps", "3", "--warmup", "3")
+    assert r.returncode != 0
+    assert "CUDA device" in r.stderr
+
+
+def test_world_size_must_match_gpus_flag():
+    e = dict(os.environ, RANK="0", LOCAL_RANK="0", WORLD_SIZE="2")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "4",
+                        "--steps", "3", "--warmup", "3"], capture_output=True, text=True,
+                       env=e, timeout=300)
+    assert r.returncode == 2 and "WORLD_SIZE" in r.stderr
+
+
+def test_reference_arm_reports_n_gpus():
+    r = _bench("--impl", "reference", "--gpus", "2", "--workload", "512", "--steps", "1",
+               "--warmup", "3", "--ref-budget", "0.3")
+    assert r.returncode == 0, r.stderr
+    d = json.loads(r.stdout.strip().splitlines()[-1])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert d["config"]["key"] == "512" and "host_cpu" in d["config"]

@@ -426,6 +426,48 @@ def test_wavefront_trace_dependency_order(rng):
             done.add((i, j))
 
 
+@pytest.mark.parametrize("shape,tile,bins", [((50, 70), 16, 4), ((1, 1), 1, 1), ((33, 17), 1, 3),
+                                             ((61, 97), 7, 16), ((193, 257), 64, 64),
+                                             ((40, 40), 1000, 256), ((130, 300), 33, 37)])
+def test_wavefront_kernel_real_trace(rng, shape, tile, bins):
+    """K7 (the wavefront as scheduled on the device): tensor bit-identical to the
+    oracle, and the recorded events are a real interleaving -- a permutation
+    of 0..2n-1 in which every tile starts after its upper and left neighbours
+    finished (strategies.py:180-181 contract)."""
+    H, W = shape
+    px = rng.integers(0, 256, shape, dtype=np.uint8)
+    lut = O.np_uniform_table(bins)
+    counts, ev = device.wavefront(device.upload_image(px), lut, bins, tile)
+    assert np.array_equal(counts.cpu().numpy(), O.compute_sequential(px, lut, bins))
+    ni, nj = -(-H // tile), -(-W // tile)
+    e = ev.cpu().numpy()
+    assert e.shape == (ni * nj, 2)
+    assert sorted(e.ravel().tolist()) == list(range(2 * ni * nj))
+    s, f = e[:, 0].reshape(ni, nj), e[:, 1].reshape(ni, nj)
+    assert (f > s).all()
+    assert (s[1:, :] > f[:-1, :]).all() and (s[:, 1:] > f[:, :-1]).all()
+
+
+def test_wavefront_trace_is_recorded_not_synthesised(rng):
+    """The trace of a wide image shows tiles of one anti-diagonal overlapping in
+    time (a synthesised per-diagonal start*/finish* list never interleaves a
+    later diagonal's start before an earlier diagonal's last finish)."""
+    px = rng.integers(0, 256, (64, 1024), dtype=np.uint8)
+    trace = []
+    t = ih.compute_wavefront(ih.GrayImage(px), ih.BinSpec.uniform(8), 8, trace=trace)
+    assert np.array_equal(t.counts, O.compute_sequential(px, O.np_uniform_table(8), 8))
+    pos = {(k, i, j): n for n, (k, i, j) in enumerate(trace)}
+    ni, nj = 8, 128
+    diag_last_finish = {}
+    for (k, i, j), n in pos.items():
+        if k == "finish":
+            d = i + j
+            diag_last_finish[d] = max(diag_last_finish.get(d, -1), n)
+    overlapped = sum(1 for (k, i, j), n in pos.items()
+                     if k == "start" and i + j > 0 and n < diag_last_finish[i + j - 1])
+    assert overlapped > 0
+
+
 def test_native_library_is_the_one_loaded():
     from paper_1711_01919_b200 import _native
 
