@@ -6,6 +6,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <unistd.h>
+
 #include <mutex>
 #include <unordered_map>
 #include <utility>
@@ -38,7 +40,41 @@ int64_t env_int(const char* name, int64_t dflt) {
   return strtoll(v, nullptr, 10);
 }
 
-constexpr int kNumSMs = 148;
+// SMs of the current device (cudaDevAttrMultiProcessorCount, cached per
+// device): the wave planner and the grid caps use the real count, so MIG
+// slices, green contexts and other SKUs plan for what they have.  148 (B200)
+// only when no device is present (ih_workspace_bytes on a CPU host).
+int device_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) {
+    cudaGetLastError();
+    return 148;
+  }
+  if (cache[dev] > 0) return cache[dev];
+  int n = 0;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    return 148;
+  }
+  cache[dev] = n;
+  return n;
+}
+
+// The IH_* tuning knobs are read from the environment (tests and A/B scripts
+// set them per call).  One pass over environ fingerprints them; plans and the
+// per-call knobs are cached under that fingerprint, so a steady stream of
+// calls costs a hash lookup instead of ~15 getenv and an occupancy query.
+uint64_t knob_fingerprint() {
+  uint64_t h = 1469598103934665603ull;
+  for (char** e = environ; e && *e; ++e) {
+    const char* s = *e;
+    if (s[0] != 'I' || s[1] != 'H' || s[2] != '_') continue;
+    for (; *s; ++s) h = (h ^ (uint8_t)*s) * 1099511628211ull;
+    h = (h ^ 0x1f) * 1099511628211ull;
+  }
+  return h;
+}
 
 // Row-segment hints (ih_plan_hint): measured segment counts per problem shape,
 // set by an autotuner; consulted by plan_k2 before its own heuristic.
@@ -50,6 +86,7 @@ constexpr int32_t kHintCluster = 1;  // ih_plan_hint flags: cluster (DSMEM) carr
 constexpr int kMaxHints = 64;
 PlanHint g_hints[kMaxHints];
 int g_nhints = 0;
+uint32_t g_hint_gen = 0;  // bumped by ih_plan_hint: invalidates cached plans
 std::mutex g_hint_mu;
 
 unsigned long long* g_trace = nullptr;  // ih_debug_trace
@@ -233,7 +270,7 @@ int ctas_per_sm(const K2Plan& p) {
   return n < 1 ? 1 : n;
 }
 
-K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma) {
+K2Plan plan_k2_uncached(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma) {
   K2Plan p;
   p.vec = vec;
   p.tma = tma;
@@ -290,7 +327,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   // quarter wave, ~2 waves (8 for the 1024-thread variant) otherwise.  If
   // the minimum segment height caps the count, snap down to whole waves.
   // Each segment costs a u16 count slot of 1/(2S) of the output (mostly L2).
-  const int64_t slots = (int64_t)kNumSMs * ctas_per_sm(p);
+  const int64_t slots = (int64_t)device_sms() * ctas_per_sm(p);
   const int64_t units = frames * p.ngroups * p.T;
   // 32-row minimum segments; 16 for short images, 8 up to 512 rows (single
   // 512^2 x 32 frame: 24.0 -> 18.7 -> 16.7 us/call graph-timed; 384^2 17.7 ->
@@ -304,7 +341,7 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   if (w_env > 0) waves = w_env / 10.0;
   const double raw = waves * (double)slots / (double)units;
   int64_t nseg;
-  if (raw <= (double)max_seg && (slots == kNumSMs || (p.colt && !many))) {
+  if (raw <= (double)max_seg && (slots == device_sms() || (p.colt && !many))) {
     // one CTA per SM, or few waves of column tiles: a partial last wave idles
     // whole SMs for a CTA's lifetime; pick the count in [raw/2, 2*raw] that
     // leaves the fewest idle slots (ties: fewer segments)
@@ -377,6 +414,78 @@ K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma)
   return p;
 }
 
+// Plan cache: (knob fingerprint, hint generation, device, shape, alignment).
+struct PlanKey {
+  uint64_t fp;
+  uint32_t gen;
+  int dev;
+  int64_t frames, H, W;
+  int nb;
+  bool vec, tma;
+  bool operator==(const PlanKey& o) const {
+    return fp == o.fp && gen == o.gen && dev == o.dev && frames == o.frames && H == o.H &&
+           W == o.W && nb == o.nb && vec == o.vec && tma == o.tma;
+  }
+};
+struct PlanKeyHash {
+  size_t operator()(const PlanKey& k) const {
+    uint64_t h = k.fp ^ ((uint64_t)k.gen << 32) ^ (uint64_t)(uint32_t)k.dev;
+    for (int64_t v : {k.frames, k.H, k.W, (int64_t)k.nb * 4 + k.vec * 2 + k.tma})
+      h = (h ^ (uint64_t)v) * 1099511628211ull;
+    return (size_t)h;
+  }
+};
+
+K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma, uint64_t fp) {
+  static std::mutex mu;
+  static std::unordered_map<PlanKey, K2Plan, PlanKeyHash> cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) {
+    cudaGetLastError();
+    dev = -1;
+  }
+  uint32_t gen;
+  {
+    std::lock_guard<std::mutex> lock(g_hint_mu);
+    gen = g_hint_gen;
+  }
+  const PlanKey key{fp, gen, dev, frames, H, W, nb, vec, tma};
+  {
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+  }
+  const K2Plan p = plan_k2_uncached(frames, H, W, nb, vec, tma);
+  std::lock_guard<std::mutex> lock(mu);
+  if (cache.size() >= 4096) cache.clear();
+  cache.emplace(key, p);
+  return p;
+}
+K2Plan plan_k2(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma) {
+  return plan_k2(frames, H, W, nb, vec, tma, knob_fingerprint());
+}
+
+// Per-call knobs, re-read only when the IH_* environment changes.
+struct Knobs {
+  uint64_t fp = 0;
+  bool valid = false;
+  bool no_pdl = false, no_tma = false, colcounts_slab = false;
+  int64_t table_sum_max = 24;
+};
+const Knobs& knobs() {
+  thread_local Knobs k;
+  const uint64_t fp = knob_fingerprint();
+  if (!k.valid || k.fp != fp) {
+    k.fp = fp;
+    k.valid = true;
+    k.no_pdl = env_int("IH_NO_PDL", 0) != 0;
+    k.no_tma = env_int("IH_NO_TMA", 0) != 0;
+    k.colcounts_slab = env_int("IH_COLCOUNTS_SLAB", 0) != 0;
+    k.table_sum_max = env_int("IH_TABLE_SUM_MAX", 24);
+  }
+  return k;
+}
+
 int resolve_kernel(int kernel, const K2Plan& p) {
   if (kernel == IH_KERNEL_AUTO) return p.cpl ? IH_KERNEL_SINGLE_PASS : IH_KERNEL_CROSSWEAVE;
   return kernel;
@@ -386,7 +495,7 @@ int resolve_kernel(int kernel, const K2Plan& p) {
 // segment s sums the s count slots above it (L2-resident, 4 slots in flight).
 // u16 prefixes need H <= 65535; taller images always sum counts in the scan.
 bool table_prefix_h(const K2Plan& p, int64_t H) {
-  return H <= 65535 && p.nseg > env_int("IH_TABLE_SUM_MAX", 24);
+  return H <= 65535 && p.nseg > knobs().table_sum_max;
 }
 
 // Workspace layouts.
@@ -454,8 +563,9 @@ ih_status validate(const uint8_t* img, int64_t frames, int64_t H, int64_t W, int
   if (frames > 65535) return fail(IH_ERR_PARAM, "at most 65535 frames per call");
   if (kernel < IH_KERNEL_AUTO || kernel > IH_KERNEL_CROSSWEAVE)
     return fail(IH_ERR_PARAM, "unknown kernel");
+  const Knobs& kn = knobs();
   c->img = img;
-  c->pdl_ok = env_int("IH_NO_PDL", 0) == 0;
+  c->pdl_ok = !kn.no_pdl;
   c->frames = frames;
   c->H = H;
   c->W = W;
@@ -469,8 +579,8 @@ ih_status validate(const uint8_t* img, int64_t frames, int64_t H, int64_t W, int
   // TMA bulk copies need 16-byte aligned rows; a row copy reads round_up(W, 16)
   // bytes, which stays inside the pitched row because pitch % 16 == 0.
   const bool tma = (uintptr_t)img % 16 == 0 && pitch % 16 == 0 && c->fstride % 16 == 0 &&
-                   env_int("IH_NO_TMA", 0) == 0;
-  c->plan = plan_k2(frames, H, W, c->nb, W % 4 == 0, tma);
+                   !kn.no_tma;
+  c->plan = plan_k2(frames, H, W, c->nb, W % 4 == 0, tma, kn.fp);
   c->kernel = resolve_kernel(kernel, c->plan);
   if (c->kernel == IH_KERNEL_SINGLE_PASS && c->plan.cpl == 0)
     return fail(IH_ERR_PARAM, "single-pass kernel without column tiles supports width <= 8192; use crossweave");
@@ -511,7 +621,7 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
                        ? (uint32_t*)((uint8_t*)ws + k2_table_bytes(c.frames, p) +
                                      k2_rowleft_bytes(c.frames, c.H, p))
                        : nullptr;
-  if (env_int("IH_COLCOUNTS_SLAB", 0) == 0) {  // all bins in one pass (shared atomics)
+  if (!knobs().colcounts_slab) {  // all bins in one pass (shared atomics)
     dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
     auto kern = al ? ih::k2_colcounts_all<true> : ih::k2_colcounts_all<false>;
     const size_t smem = (size_t)(p.nbp + 1) * 64 * sizeof(uint32_t);
@@ -546,7 +656,7 @@ ih_status launch_colprefix(const Call& c, void* ws) {
   if (!table_prefix_h(p, c.H)) return IH_OK;  // the scan kernel sums the count slots
   const int64_t total = c.frames * p.nbp * p.Wp / 4 * ih::kPrefixLanes;  // 8 lanes per quad
   int64_t blocks = (total + 255) / 256;
-  if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+  if (blocks > device_sms() * 16) blocks = device_sms() * 16;
   if (launch(ih::k2_colprefix, dim3((unsigned)blocks), dim3(256), 0, c.stream, c.pdl(),
              (uint16_t*)ws, c.frames, p.nseg, p.nbp, p.Wp) != cudaSuccess)
     return cuda_fail("k2_colprefix");
@@ -601,7 +711,7 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
     const int64_t planes = c.frames * c.nb;
     const int64_t per = vec ? c.W / 4 : c.W;
     int64_t blocks = (planes * per + 255) / 256;
-    if (blocks > kNumSMs * 32) blocks = kNumSMs * 32;
+    if (blocks > device_sms() * 32) blocks = device_sms() * 32;
     if (c.H > 1) {
       if (vec) ih::k1b_colscan<true><<<(unsigned)blocks, 256, 0, c.stream>>>(out, planes, c.H, c.W);
       else ih::k1b_colscan<false><<<(unsigned)blocks, 256, 0, c.stream>>>(out, planes, c.H, c.W);
@@ -661,9 +771,10 @@ size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width, int32_t
   // the plan depends on the input alignment (1024-thread variants need the TMA
   // path); size the workspace for either
   size_t n = 0;
+  const uint64_t fp = knob_fingerprint();
   for (int variant = 0; variant < 4; ++variant) {
     K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0 && (variant & 1),
-                       (variant & 2) != 0);
+                       (variant & 2) != 0, fp);
     if (resolve_kernel(kernel, p) != IH_KERNEL_SINGLE_PASS || p.cpl == 0) continue;
     const size_t b = k2_ws_bytes(frames, height, p);
     if (b > n) n = b;
@@ -718,7 +829,7 @@ ih_status ih_region_histograms(const uint32_t* t, int32_t nb, int64_t height, in
   if (!t || !regions || !out) return fail(IH_ERR_PARAM, "null pointer");
   if ((uintptr_t)regions % 16 != 0) return fail(IH_ERR_PARAM, "regions must be 16-byte aligned");
   int64_t blocks = (q + 7) / 8;  // 8 warps per CTA, one query per warp
-  if (blocks > kNumSMs * 64) blocks = kNumSMs * 64;
+  if (blocks > device_sms() * 64) blocks = device_sms() * 64;
   ih::k3_region_histograms<<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
       t, nb, height, width, reinterpret_cast<const int4*>(regions), q,
       reinterpret_cast<unsigned long long*>(out));
@@ -749,7 +860,7 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
     const int64_t cb = (C + 1 + 2 * 256 * U - 1) / (2 * 256 * U);  // U pairs per thread
     // grid-strided rows, ~256 CTAs' worth per SM (measured best: HD x32 64x64
     // windows 0.164 -> 0.148 ms vs mode 1; profiles/r01f/queries_k4_pairs.jsonl)
-    int64_t ry = (int64_t)kNumSMs * env_int("IH_K4_CTAS_PER_SM", 256) / (cb * nb);
+    int64_t ry = (int64_t)device_sms() * env_int("IH_K4_CTAS_PER_SM", 256) / (cb * nb);
     ry = ry < 1 ? 1 : ry > R ? R : ry > 65535 ? 65535 : ry;
     dim3 grid((unsigned)cb, (unsigned)ry, (unsigned)nb);
     auto k = U == 4 ? ih::k4_window_counts_pairs<4> : U == 1 ? ih::k4_window_counts_pairs<1>
@@ -764,7 +875,7 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
     // several rows (one-row CTAs: 0.52 of HBM, 148*64 CTAs: 0.59, HD x32;
     // with u32 window arithmetic and <= 40 registers: 0.70)
     const int64_t cb = (C + 1023) / 1024;
-    int64_t ry = (int64_t)kNumSMs * 64 / (cb * nb);
+    int64_t ry = (int64_t)device_sms() * 64 / (cb * nb);
     ry = ry < 1 ? 1 : ry > R ? R : ry > 65535 ? 65535 : ry;
     ry = env_int("IH_K4_ROWS_GRID", ry);
     dim3 grid((unsigned)cb, (unsigned)ry, (unsigned)nb);
@@ -807,7 +918,7 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   if (kernel < IH_KERNEL_AUTO || kernel > IH_KERNEL_CROSSWEAVE)
     return fail(IH_ERR_PARAM, "unknown kernel");
   if (!info) return fail(IH_ERR_PARAM, "null info pointer");
-  const bool tma = aligned16 != 0 && env_int("IH_NO_TMA", 0) == 0;
+  const bool tma = aligned16 != 0 && !knobs().no_tma;
   K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0, tma);
   const int k = resolve_kernel(kernel, p);
   for (int i = 0; i < 14; ++i) info[i] = 0;
@@ -868,7 +979,7 @@ ih_status ih_likelihood_map_ws(const uint32_t* t, int32_t nb, int64_t height, in
     double* M = (double*)workspace;
     const int64_t total = (int64_t)nb * ((int64_t)h * w + 1);
     int64_t blocks = (total + 255) / 256;
-    if (blocks > kNumSMs * 16) blocks = kNumSMs * 16;
+    if (blocks > device_sms() * 16) blocks = device_sms() * 16;
     if (metric == IH_METRIC_INTERSECTION)
       ih::k5_metric_table<true><<<(unsigned)blocks, 256, 0, (cudaStream_t)stream>>>(
           tpl, nb, (int64_t)h * w, M);
@@ -927,10 +1038,12 @@ ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t sl
       } else {
         h = g_hints[--g_nhints];
       }
+      ++g_hint_gen;
       return IH_OK;
     }
   }
   if (nseg == 0) return IH_OK;
+  ++g_hint_gen;
   if (g_nhints == kMaxHints) g_nhints = 0;  // a small cache: start over when full
   g_hints[g_nhints++] = PlanHint{frames, height, width, slab_bins, nseg, tail_pct, tail_div, flags};
   return IH_OK;
