@@ -103,14 +103,47 @@ def measured_peaks():
         return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def committed_traffic(wl: Workload):
+def committed_traffic(wl: Workload, plan: dict):
     """dram__bytes_read.sum + dram__bytes_write.sum per histogram of k2_scan from
-    the committed ncu --set full capture (profiles/ncu_traffic.json), or None."""
+    the committed ncu --set full capture (profiles/ncu_traffic.json), or None
+    when there is none for this workload or it was taken with a different
+    launch plan (segments / column tiles) than the one this run uses."""
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
-            return json.load(fh)["per_histogram"][wl.key]["bytes"]
+            e = json.load(fh)["per_histogram"][wl.key]
     except Exception:
         return None
+    if e.get("segments") != plan.get("segments") or \
+            e.get("column_tiles", 1) != plan.get("column_tiles", 1):
+        return None
+    return e["bytes"]
+
+
+CSV_EXTRA = "devices,alg_bytes,gbs,frac_of_peak,ncu_dram_bytes,host_cpu"
+
+
+def write_csv(path: str, line: dict, wl: Workload) -> None:
+    """Append the run as one row of the reference's CSV schema
+    (pkg/src/inthist/bench.py:24) plus the BASELINE.md 4.5 roofline columns;
+    per-histogram figures (median_ms = 1000 / aggregate hist/s)."""
+    from paper_1711_01919_b200.harness import CSV_HEADER
+
+    new = not os.path.exists(path)
+    v = line["value"]
+    ms = 1000.0 / v
+    crc = golden().get(f"{wl.width}x{wl.height}x{wl.bins}", {}).get("crc", "")
+    tr = line["roofline"].get("traffic")
+    hists = line["config"]["histograms_per_step"]
+    row = [line.get("impl", "single_pass"), wl.width, wl.height, wl.bins, 0, 0, line["steps"],
+           f"{ms:.6f}", f"{ms:.6f}", f"{v:.6f}", crc if line.get("parity", "").startswith(
+               ("rank-0 output crc32 ==", "output crc32 ==")) else "",
+           line["n_gpus"], wl.alg_bytes, f"{v * wl.alg_bytes / 1e9:.1f}",
+           f"{line['hbm_frac_step']:.4f}", f"{tr / hists:.0f}" if tr else "",
+           '"' + line["config"]["host_cpu"] + '"']
+    with open(path, "a") as fh:
+        if new:
+            fh.write(CSV_HEADER + "," + CSV_EXTRA + "\n")
+        fh.write(",".join(str(x) for x in row) + "\n")
 
 
 def golden():
@@ -533,7 +566,7 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     peak, peak_src = measured_peaks()
     alg_launch = nloc * (wl.width * wl.height + 256 + 4 * nb * wl.width * wl.height)
     achieved = alg_launch / (scan_ms / 1000.0) / 1e9
-    traffic = committed_traffic(wl)
+    traffic = committed_traffic(wl, plan)
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -555,6 +588,9 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
         "parity": "rank-0 output crc32 == reference golden" if not bad else "MISMATCH",
         "clocks": clocks.summary(),
     }
+    if traffic is None:
+        line["roofline"]["traffic_note"] = ("no committed ncu capture of this workload with "
+                                            "this launch plan (profiles/ncu_traffic.json)")
     if gather_ms is not None:
         line["gather_ms"] = gather_ms
     if queries is not None:
@@ -566,6 +602,8 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": sample}
     print(json.dumps(line), flush=True)
+    if args.csv:
+        write_csv(args.csv, line, wl)
 
 
 def run_small(args, wl: Workload, rank, world, local_rank):
@@ -725,6 +763,8 @@ def run_small(args, wl: Workload, rank, world, local_rank):
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cores, "kind": "port",
                                 "sample": sample}
     print(json.dumps(line), flush=True)
+    if args.csv:
+        write_csv(args.csv, line, wl)
 
 
 def run_e2e(args, wl, spec, host, nloc, brange, out, dev, barrier, reduce_max, world):
@@ -786,6 +826,8 @@ def main():
                     help="run each step's prepass and scan back to back on one stream")
     ap.add_argument("--ref-budget", type=float, default=10.0,
                     help="seconds of CPU work per reference sample (bounded)")
+    ap.add_argument("--csv", default="",
+                    help="also append the run to this CSV (reference schema + roofline columns)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launcher / partition / max-over-ranks plumbing only (no GPU work; "
                          "CPU tests of the N>1 path)")

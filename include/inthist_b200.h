@@ -238,6 +238,15 @@ const char *ih_last_error(void);
 /* ABI version: (major << 16) | minor. */
 int32_t ih_abi_version(void);
 
+/* Page-locked host buffer for D2H of large results (cudaHostAlloc), owned by
+ * the caller and released with ih_host_free -- unlike a caching host
+ * allocator, the pages go back to the OS when the result is dropped.  NULL on
+ * failure (no device, or the pages cannot be locked).  No reference
+ * counterpart: the reference keeps its tensor in host memory
+ * (IntegralHistogram.counts, core.py:106-116). */
+void *ih_host_alloc(size_t bytes);
+void ih_host_free(void *p);
+
 #ifdef __cplusplus
 }
 #endif

@@ -50,6 +50,8 @@ EXPORTS = (
     "ih_status_string",
     "ih_last_error",
     "ih_abi_version",
+    "ih_host_alloc",
+    "ih_host_free",
 )
 
 _lib = None
@@ -113,6 +115,10 @@ def lib() -> ctypes.CDLL:
     L.ih_last_error.restype = ctypes.c_char_p
     L.ih_abi_version.argtypes = []
     L.ih_abi_version.restype = i32
+    L.ih_host_alloc.argtypes = [sz]
+    L.ih_host_alloc.restype = P
+    L.ih_host_free.argtypes = [P]
+    L.ih_host_free.restype = None
     _lib = L
     return L
 

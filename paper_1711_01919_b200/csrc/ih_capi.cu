@@ -1202,6 +1202,19 @@ const char* ih_status_string(ih_status s) {
 
 const char* ih_last_error(void) { return g_last_error; }
 
-int32_t ih_abi_version(void) { return (1 << 16) | 5; }
+int32_t ih_abi_version(void) { return (1 << 16) | 6; }
+
+void* ih_host_alloc(size_t bytes) {
+  void* p = nullptr;
+  if (bytes == 0 || cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void ih_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
 
 }  // extern "C"

@@ -12,6 +12,7 @@ synchronise the host.
 
 from __future__ import annotations
 
+import contextlib
 import ctypes
 import os
 
@@ -22,13 +23,20 @@ from . import _native
 from .errors import BoundsError, DeviceError, ParameterError, ShapeError
 
 _workspaces: dict[int, torch.Tensor] = {}
+_cuda_seen = False  # a CUDA device was visible once (availability cannot go away)
+_NULLCTX = contextlib.nullcontext()
 
 
 def require_cuda(device=None) -> torch.device:
     """The CUDA device to run on; raises DeviceError when none exists (no CPU fallback)."""
-    if not torch.cuda.is_available():
-        raise DeviceError("no CUDA device visible: the B200 engine has no CPU fallback")
-    _native.lib()
+    global _cuda_seen
+    if not _cuda_seen:
+        if not torch.cuda.is_available():
+            raise DeviceError("no CUDA device visible: the B200 engine has no CPU fallback")
+        _native.lib()
+        _cuda_seen = True
+    if isinstance(device, torch.device) and device.type == "cuda" and device.index is not None:
+        return device  # the common case: a tensor's device
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
     if dev.type != "cuda":
         raise DeviceError(f"expected a CUDA device, got {dev}")
@@ -38,8 +46,18 @@ def require_cuda(device=None) -> torch.device:
 
 
 def _stream_handle(dev: torch.device, stream=None) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream(dev)
-    return int(s.cuda_stream)
+    if stream is not None:
+        return int(stream.cuda_stream)
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:  # the handle without building a Stream object
+        return int(raw(dev.index))
+    return int(torch.cuda.current_stream(dev).cuda_stream)
+
+
+def _on_device(dev: torch.device):
+    """Context making `dev` current for the C ABI's launches (a no-op when it
+    already is: entering torch.cuda.device costs microseconds per call)."""
+    return _NULLCTX if torch.cuda.current_device() == dev.index else torch.cuda.device(dev)
 
 
 def workspace_(dev: torch.device, nbytes: int) -> torch.Tensor:
@@ -52,11 +70,26 @@ def workspace_(dev: torch.device, nbytes: int) -> torch.Tensor:
     return ws
 
 
+_lut_last: list = [None, 0]  # [last uint8 table array (kept alive), its data pointer]
+
+
 def _lut_array(table) -> np.ndarray:
     lut = np.ascontiguousarray(np.asarray(table), dtype=np.uint8)
     if lut.shape != (256,):
         raise ShapeError("lookup table must have exactly 256 entries")
     return lut
+
+
+def _lut_ptr(a: "_Args") -> int:
+    """Host address of the call's 256-byte table (read by the C ABI during the
+    call).  A table that already is a contiguous uint8 array is used in place,
+    so its pointer is cached per table object."""
+    lut = a.lut
+    if _lut_last[0] is lut:
+        return _lut_last[1]
+    ptr = lut.ctypes.data
+    _lut_last[0], _lut_last[1] = lut, ptr
+    return ptr
 
 
 def _frames_view(images: torch.Tensor):
@@ -361,9 +394,9 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
             raise ShapeError("out has the wrong size or device")
     ws = _workspace_for(a, workspace)
     L = _native.lib()
-    with torch.cuda.device(a.dev):  # launches go to the tensors' device
+    with _on_device(a.dev):  # launches go to the tensors' device
         _native.check(L.ih_integral_histogram(
-            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, _lut_ptr(a),
             a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
             a.kernel, a.stream))
     if squeeze and out.dim() == 4:
@@ -389,9 +422,9 @@ def prepare(images, table, bins, bin_range=None, kernel="auto", stream=None,
     scan (write-bound) runs."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
     ws = _workspace_for(a, workspace)
-    with torch.cuda.device(a.dev):
+    with _on_device(a.dev):
         _native.check(_native.lib().ih_ih_prepare(
-            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, _lut_ptr(a),
             a.bins, a.lo, a.hi, ws.data_ptr(), ws.numel() * ws.element_size(), a.kernel,
             a.stream))
 
@@ -401,9 +434,9 @@ def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None,
     """Phase 2 of integral_histogram (the dominant single-pass kernel)."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
     ws = _workspace_for(a, workspace)
-    with torch.cuda.device(a.dev):
+    with _on_device(a.dev):
         _native.check(_native.lib().ih_ih_scan(
-            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, a.lut.ctypes.data,
+            a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, _lut_ptr(a),
             a.bins, a.lo, a.hi, out.data_ptr(), ws.data_ptr(), ws.numel() * ws.element_size(),
             a.kernel, a.stream))
     return out
@@ -561,26 +594,49 @@ def likelihood_map(t: torch.Tensor, template, h: int, w: int, metric: str = "bha
 
 
 PINNED_MIN_BYTES = 1 << 20
+PRIVATE_PINNED_MIN_BYTES = 1 << 30
 _VIEW_AS = {torch.uint32: (torch.int32, np.uint32), torch.uint64: (torch.int64, np.uint64)}
+
+
+def _private_pinned(shape, dtype: torch.dtype):
+    """A host tensor in its own page-locked allocation (ih_host_alloc), freed
+    (ih_host_free) when the last numpy/torch view of it is garbage-collected;
+    None if the pages cannot be locked."""
+    import weakref
+
+    nbytes = int(np.prod(shape)) * torch.empty((), dtype=dtype).element_size()
+    L = _native.lib()
+    ptr = L.ih_host_alloc(nbytes)
+    if not ptr:
+        return None
+    raw = (ctypes.c_uint8 * nbytes).from_address(ptr)
+    weakref.finalize(raw, L.ih_host_free, ptr)
+    flat = np.frombuffer(raw, dtype=np.uint8)  # keeps `raw` alive
+    return torch.from_numpy(flat).view(dtype).view(shape)
 
 
 def to_host(t: torch.Tensor) -> np.ndarray:
     """D2H of a device result into a numpy array of the same dtype.
 
-    Results of 1 MB and more land in page-locked memory from torch's caching
-    host allocator (~55 GB/s, blocks reused across calls); a fresh pageable
-    array page-faults on first touch and the copy runs at ~2 GB/s.  The array
-    is a view that keeps its pinned block alive.  ``IH_NO_PINNED=1`` disables.
+    Results of 1 MB and more land in page-locked memory (~55 GB/s; a fresh
+    pageable array page-faults on first touch and the copy runs at ~2 GB/s):
+    below 1 GB from torch's caching host allocator (blocks reused across
+    calls), from 1 GB up in a private page-locked allocation that is returned
+    to the OS when the array dies -- a cached block would pin e.g. 68.7 GB
+    for an 8192^2 x 256 result for the life of the process.  The array is a
+    view that keeps its block alive.  ``IH_NO_PINNED=1`` disables both.
     """
-    import os
-
     src, np_view = t, None
     if t.dtype in _VIEW_AS:
         carrier, np_view = _VIEW_AS[t.dtype]
         src = t.view(carrier)
     nbytes = src.numel() * src.element_size()
+    host = None
     if nbytes >= PINNED_MIN_BYTES and os.environ.get("IH_NO_PINNED", "0") == "0":
-        host = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
+        if nbytes >= PRIVATE_PINNED_MIN_BYTES:
+            host = _private_pinned(tuple(src.shape), src.dtype)
+        if host is None:
+            host = torch.empty(src.shape, dtype=src.dtype, pin_memory=True)
         host.copy_(src)
         arr = host.numpy()
     else:

@@ -410,6 +410,29 @@ def test_streamed_equals_sequential(rng):
     assert summary.peak_bytes <= 80_000
 
 
+@pytest.mark.parametrize("budget", [40_000, 200_000, 3_000_000, 50_000_000])
+def test_streamed_overlap_paths(rng, budget):
+    """f2 overlap: single vs double staging buffers, per-plane strip copies vs
+    whole-slab copies, chunk look-ahead; the sink sees every piece in the
+    reference's order and peak_bytes is the measured staging, within budget."""
+    px = rng.integers(0, 256, (181, 203), dtype=np.uint8)
+    img, spec = ih.GrayImage(px), ih.BinSpec.uniform(48)
+    plan = ih.plan_tiles(203, 181, 48, budget)
+    order = []
+
+    class Sink(ih.ArraySink):
+        def write(self, lo, hi, r0, r1, data):
+            order.append((lo, r0))
+            super().write(lo, hi, r0, r1, data)
+
+    sink = Sink(203, 181, 48)
+    summary = ih.compute_streamed(img, spec, plan, sink)
+    assert np.array_equal(sink.counts, O.compute_crossweave(px, spec.table, 48))
+    assert order == [(lo, r0) for lo, _ in plan.bin_chunks for r0 in range(0, 181, plan.strip_height)]
+    assert summary.peak_bytes <= budget
+    assert summary.strips == len(plan.bin_chunks) * plan.strips
+
+
 def test_wavefront_trace_dependency_order(rng):
     px = rng.integers(0, 256, (50, 70), dtype=np.uint8)
     trace = []
@@ -758,3 +781,35 @@ def test_tall_and_wide_column_tiles(rng):
     got = dev_compute(px, lut, 2, kernel="single_pass")
     want = O.compute_crossweave(px, lut, 2)
     assert np.array_equal(got.cpu().numpy(), want)
+
+
+def test_to_host_private_pinned_released(monkeypatch):
+    """Results >= PRIVATE_PINNED_MIN_BYTES get their own page-locked block
+    (ih_host_alloc) that is freed when the array dies, not a cached one."""
+    import gc
+
+    freed = []
+    L = device._native.lib()
+    real_free = L.ih_host_free
+    monkeypatch.setattr(device, "PRIVATE_PINNED_MIN_BYTES", 1 << 20)
+
+    class Spy:
+        def __getattr__(self, name):
+            return getattr(L, name)
+
+        def ih_host_free(self, p):
+            freed.append(p)
+            real_free(p)
+
+    monkeypatch.setattr(device._native, "lib", lambda: Spy())
+    t = torch.arange(1 << 19, dtype=torch.int32, device="cuda").view(torch.uint32).reshape(512, 1024)
+    a = device.to_host(t)
+    assert a.dtype == np.uint32 and np.array_equal(a, np.arange(1 << 19, dtype=np.uint32).reshape(512, 1024))
+    assert not freed
+    v = a[3:5]
+    del a
+    gc.collect()
+    assert not freed and int(v[0, 0]) == 3 * 1024
+    del v
+    gc.collect()
+    assert len(freed) == 1
