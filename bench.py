@@ -113,10 +113,11 @@ def committed_traffic(wl: Workload, plan: dict):
             e = json.load(fh)["per_histogram"][wl.key]
     except Exception:
         return None
-    if e.get("segments") != plan.get("segments") or \
-            e.get("column_tiles", 1) != plan.get("column_tiles", 1):
+    if e.get("column_tiles", 1) != plan.get("column_tiles", 1) or \
+            plan.get("big_segments") != plan.get("segments"):  # captures have no tail split
         return None
-    return e["bytes"]
+    cap = e.get("by_segments", {}).get(str(plan.get("segments")))
+    return cap["bytes"] if cap else None
 
 
 CSV_EXTRA = "devices,alg_bytes,gbs,frac_of_peak,ncu_dram_bytes,host_cpu"

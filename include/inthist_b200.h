@@ -113,7 +113,9 @@ ih_status ih_ih_scan(const uint8_t *img, int64_t frames, int64_t height, int64_t
  *   info[8] column tiles per row             info[9] tile width (columns)
  *   info[10] resident scan CTAs (SMs x CTAs/SM)  info[11] scan CTAs per row segment
  *   info[12] big segments (the rest are tail segments)  info[13] tail segment rows
- * (`info` holds 14 entries.)  Same shape/parameter errors as ih_integral_histogram. */
+ *   info[14] segment carries: 0 none, 1 count table (prepass kernels), 2 look-back,
+ *            3 cluster (DSMEM), 4 in-kernel (K2s: one launch, small images)
+ * (`info` holds 15 entries.)  Same shape/parameter errors as ih_integral_histogram. */
 ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
                            int32_t kernel, int32_t aligned16, int64_t *info);
 
@@ -124,7 +126,8 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
  * segment-major scan grid runs last.  flags bit 0: carry the segments through
  * a thread-block cluster (the <= 16 segments of a strip exchange their column
  * counts in distributed shared memory: one launch, no prepass; taken when the
- * plan allows it -- no column tiles, H < 65536).  Results are identical for
+ * plan allows it -- no column tiles, H < 65536); bit 1: the K2s one-launch
+ * kernel (in-kernel carries; W <= 2048, 16-byte aligned rows, H < 65536).  Results are identical for
  * every choice; only speed changes.  nseg = 0 removes the hint.  A small
  * process-wide table guarded by a mutex; device.autotune() fills it. */
 ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,

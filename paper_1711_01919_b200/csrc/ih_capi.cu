@@ -17,6 +17,7 @@
 #include "ih_queries.cu"
 #include "ih_scan.cu"
 #include "ih_single_pass.cu"
+#include "ih_small.cu"
 #include "ih_wavefront.cu"
 
 namespace {
@@ -83,6 +84,7 @@ struct PlanHint {
   int32_t nb, nseg, tail_pct, tail_div, flags;
 };
 constexpr int32_t kHintCluster = 1;  // ih_plan_hint flags: cluster (DSMEM) carries
+constexpr int32_t kHintSmall = 2;    // ih_plan_hint flags: K2s one-launch path
 constexpr int kMaxHints = 64;
 PlanHint g_hints[kMaxHints];
 int g_nhints = 0;
@@ -147,6 +149,9 @@ struct K2Plan {
   bool big = false;  // 1024-thread instantiation (up to 32 warps, <= 64 registers)
   bool vec = true;   // W % 4 == 0
   bool tma = true;   // 16-byte aligned rows
+  bool small = false;  // K2s: one launch, in-kernel segment carries (ih_small.cu)
+  int nwg = 1;         // K2s warp-groups per CTA
+  int Sk = 0;          // K2s rows per warp-group
 };
 
 // Opt a kernel into `bytes` of dynamic shared memory.  Static + dynamic
@@ -268,6 +273,95 @@ int ctas_per_sm(const K2Plan& p) {
   const int regs = p.cpl == 1 ? 56 : p.cpl == 2 ? (p.big ? 64 : 96) : 128;
   n = 65536 / (regs * p.nwarps * 32);
   return n < 1 ? 1 : n;
+}
+
+// ---- K2s (ih_small.cu): one launch with in-kernel segment carries
+using KSFn = void (*)(ih::SmallArgs, ih::RelLut);
+KSFn pick_small(const K2Plan& p) {
+  switch (p.nwg) {
+    case 4: return p.vec ? ih::k2_small<4, true> : ih::k2_small<4, false>;
+    case 2: return p.vec ? ih::k2_small<2, true> : ih::k2_small<2, false>;
+    default: return p.vec ? ih::k2_small<1, true> : ih::k2_small<1, false>;
+  }
+}
+// staged rows: one bulk copy per warp-group when the rows are contiguous in
+// a pitch of at most twice the vector width (the smem row stride is then the
+// pitch); otherwise one copy per row at stride TW
+bool small_contig(const K2Plan& p, int64_t pitch) { return pitch <= 2 * (int64_t)p.TW; }
+size_t small_ring_bytes(const K2Plan& p, int64_t pitch) {
+  const int64_t rs = small_contig(p, pitch) ? pitch : p.TW;
+  return ((size_t)p.S * rs + p.TW + 15) / 16 * 16;
+}
+size_t small_smem(const K2Plan& p, int64_t pitch) {  // rows | cnt | psum
+  return small_ring_bytes(p, pitch) + (size_t)2 * p.nwg * 2 * p.TW * sizeof(uint32_t);
+}
+int small_ctas_per_sm(const K2Plan& p) {
+  KSFn fn = pick_small(p);
+  const size_t smem = small_smem(p, 2 * (int64_t)p.TW);  // the larger staging layout
+  int n = 0;
+  if (set_dyn_smem((const void*)fn, smem) &&
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, p.nwarps * 32, smem) == cudaSuccess &&
+      n > 0)
+    return n;
+  cudaGetLastError();
+  return 1;
+}
+// Plan K2s when one wave of CTAs covers the problem with >= 2 segments per
+// frame: W <= 2048 (one 128-column chunk per warp, <= 16 warps), 16-byte
+// aligned rows (TMA), H <= 65535 (16-bit count lanes).  `force`: hint flag /
+// IH_SMALL=1; automatically only for frames x bin groups <= 4 -- the
+// measured cases where one launch beats the count-table path (512x512x16
+// bins 16.3 vs 21.4 us graph-timed; with 8+ groups the table path's
+// 3 launches win, e.g. 512x512x32 16.8 vs 18.6 us: profiles/r02d/).
+bool plan_small(K2Plan& p, int64_t frames, int64_t H, int64_t W, int nb, bool force,
+                int64_t want_nseg) {
+  const int64_t nch = (W + ih::kChunk - 1) / ih::kChunk;
+  if (!p.tma || H > 65535 || nch > 16 || frames > 65535) return false;
+  K2Plan q = p;
+  q.small = true;
+  q.cpl = 1;
+  q.colt = false;
+  q.big = false;
+  q.staged = false;
+  q.kb = ih::kGroup;
+  q.R = 4;
+  q.T = 1;
+  q.nwg = nch <= 4 ? 4 : nch <= 8 ? 2 : 1;
+  const int wpg = (int)nch;
+  q.TW = wpg * ih::kChunk;
+  q.Wp = q.TW;
+  q.nwarps = q.nwg * wpg;
+  q.ngroups = (nb + ih::kGroup - 1) / ih::kGroup;
+  q.nbp = q.ngroups * ih::kGroup;
+  const int64_t units = frames * q.ngroups;
+  if (!force && units > 4) return false;
+  const int64_t sms = device_sms();
+  // segment count for one wave; the shared-memory size depends on S, so
+  // settle the occupancy in two rounds
+  int64_t nseg = sms / units;
+  for (int it = 0; it < 2; ++it) {
+    if (nseg < 1) nseg = 1;
+    if (nseg > H) nseg = H;
+    q.S = (int)((H + nseg - 1) / nseg);
+    q.slots = (int)(sms * small_ctas_per_sm(q));
+    nseg = q.slots / units;
+  }
+  // >= one 4-row batch per warp-group (unless forced)
+  const int64_t max_seg = force ? H : H / (4 * q.nwg);
+  if (nseg > max_seg) nseg = max_seg;
+  if (nseg < 2 && !force) return false;  // frames x groups already fill a wave
+  if (force && want_nseg > 0) nseg = want_nseg < H ? want_nseg : H;  // hint / IH_NSEG
+  if (nseg < 1) nseg = 1;
+  q.S = (int)((H + nseg - 1) / nseg);
+  q.nseg = (int)((H + q.S - 1) / q.S);
+  q.Sk = (q.S + q.nwg - 1) / q.nwg;
+  q.nbig = q.nseg;
+  q.S2 = q.S;
+  q.units = units;
+  q.carry = ih::CARRY_NONE;
+  if (small_smem(q, 2 * (int64_t)q.TW) > 200 * 1024) return false;
+  p = q;
+  return true;
 }
 
 K2Plan plan_k2_uncached(int64_t frames, int64_t H, int64_t W, int nb, bool vec, bool tma) {
@@ -411,6 +505,17 @@ K2Plan plan_k2_uncached(int64_t frames, int64_t H, int64_t W, int nb, bool vec, 
   else if (p.colt) p.carry = ih::CARRY_TABLE;
   else p.carry = env_int("IH_CARRY_LOOKBACK", 0) ? ih::CARRY_LOOKBACK : ih::CARRY_TABLE;
   if (p.carry == ih::CARRY_LOOKBACK || p.carry == ih::CARRY_CLUSTER) p.staged = false;
+  // K2s for images that one wave of CTAs covers: automatic unless a knob or a
+  // hint chose the segmentation / carry scheme; IH_SMALL=1 or the hint flag
+  // force it where it applies, IH_SMALL=0 disables it
+  const int64_t small_env = env_int("IH_SMALL", -1);
+  const bool auto_mode = hinted <= 0 && forced <= 0 && env_int("IH_TAIL_PCT", 0) == 0 &&
+                         !want_cluster && env_int("IH_CARRY_LOOKBACK", 0) == 0 &&
+                         env_int("IH_STAGED_STORES", 0) == 0 && env_int("IH_COLCOUNTS_SLAB", 0) == 0 &&
+                         env_int("IH_MIN_SEG_ROWS", 0) == 0 && env_int("IH_TARGET_WAVES_X10", 0) == 0;
+  const bool force_small = small_env == 1 || (hinted_flags & kHintSmall);
+  if (small_env != 0 && (force_small || auto_mode) && p.cpl == 1 && !p.colt)
+    plan_small(p, frames, H, W, nb, force_small, forced > 0 ? forced : hinted);
   return p;
 }
 
@@ -520,7 +625,16 @@ size_t k2_chunktot_bytes(int64_t frames, const K2Plan& p) {
   if (!p.colt || p.T < 2 || p.carry != ih::CARRY_TABLE) return 0;
   return (size_t)frames * p.nseg * (p.Wp / ih::kChunk) * p.nbp * sizeof(uint32_t);
 }
+//   K2s (small):    [pad 16 B][flags: tiles u32, 16 B padded]
+//                   [aggregates: tiles x 2 x TW u32], tiles = frames x groups x nseg
+int64_t small_tiles(int64_t frames, const K2Plan& p) { return frames * p.ngroups * p.nseg; }
+size_t small_header_bytes(int64_t frames, const K2Plan& p) {
+  return 16 + (size_t)((small_tiles(frames, p) * 4 + 15) / 16 * 16);
+}
 size_t k2_ws_bytes(int64_t frames, int64_t H, const K2Plan& p) {
+  if (p.small)
+    return small_header_bytes(frames, p) +
+           (size_t)small_tiles(frames, p) * 2 * p.TW * sizeof(uint32_t);
   if (p.colt)
     return k2_table_bytes(frames, p) + k2_rowleft_bytes(frames, H, p) + k2_chunktot_bytes(frames, p);
   if (p.carry == ih::CARRY_TABLE) return (size_t)frames * p.nseg * p.nbp * p.Wp * sizeof(uint16_t);
@@ -601,6 +715,11 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
   if (need == 0) return IH_OK;
   if (ws_bytes < need || !ws)
     return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
+  if (p.small) {  // K2s: reset the aggregate flags
+    if (cudaMemsetAsync(ws, 0, small_header_bytes(c.frames, p), c.stream) != cudaSuccess)
+      return cuda_fail("K2s flag reset");
+    return IH_OK;
+  }
   if (p.colt && p.T > 1) {  // row counts left of each tile boundary
     uint32_t* lc = (uint32_t*)((uint8_t*)ws + k2_table_bytes(c.frames, p));
     dim3 grid((unsigned)((c.H + ih::kRowLeftWarps - 1) / ih::kRowLeftWarps), (unsigned)c.frames);
@@ -722,6 +841,39 @@ ih_status launch_scan(const Call& c, uint32_t* out, void* ws, size_t ws_bytes) {
   const K2Plan& p = c.plan;
   if (k2_ws_bytes(c.frames, c.H, p) > 0 && (ws_bytes < k2_ws_bytes(c.frames, c.H, p) || !ws))
     return fail(IH_ERR_PARAM, "workspace too small (see ih_workspace_bytes)");
+  if (p.small) {
+    ih::SmallArgs a;
+    a.img = c.img;
+    a.H = c.H;
+    a.W = c.W;
+    a.pitch = c.pitch;
+    a.fstride = c.fstride;
+    a.nb = c.nb;
+    a.ngroups = p.ngroups;
+    a.nseg = p.nseg;
+    a.S = p.S;
+    a.Sk = p.Sk;
+    a.wpg = p.nwarps / p.nwg;
+    a.TWp = p.TW;
+    a.contig = small_contig(p, c.pitch) ? 1 : 0;
+    a.RS = a.contig ? (int)c.pitch : p.TW;
+    a.row_bytes = (uint32_t)((c.W + 15) / 16 * 16);
+    uint8_t* base = (uint8_t*)ws;
+    a.flags = (uint32_t*)(base + 16);
+    a.agg = (uint32_t*)(base + small_header_bytes(c.frames, p));
+    a.out = out;
+    const int64_t tiles = small_tiles(c.frames, p);
+    a.trace = (g_trace && 2 * (size_t)tiles <= g_trace_ctas) ? g_trace : nullptr;
+    KSFn fn = pick_small(p);
+    const size_t smem = small_smem(p, c.pitch);
+    if (!set_dyn_smem((const void*)fn, smem)) return cuda_fail("k2_small smem attribute");
+    // after the flag memset: no PDL
+    if (launch(fn, dim3((unsigned)tiles), dim3(p.nwarps * 32), smem, c.stream, false, a, c.lut) !=
+        cudaSuccess)
+      return cuda_fail("k2_small");
+    ++c.launched;
+    return IH_OK;
+  }
   ih::ScanArgs a;
   a.img = c.img;
   a.H = c.H;
@@ -921,14 +1073,14 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   const bool tma = aligned16 != 0 && !knobs().no_tma;
   K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0, tma);
   const int k = resolve_kernel(kernel, p);
-  for (int i = 0; i < 14; ++i) info[i] = 0;
+  for (int i = 0; i < 15; ++i) info[i] = 0;
   info[0] = k;
   if (k == IH_KERNEL_CROSSWEAVE) {
     info[1] = height > 1 ? 2 : 1;
     return IH_OK;
   }
   if (p.cpl == 0) return fail(IH_ERR_PARAM, "single-pass kernel supports width <= 8192");
-  int launches = 1;
+  int launches = 1;  // K2s: one kernel (after a memset of its flags)
   if (p.carry == ih::CARRY_TABLE) launches += table_prefix_h(p, height) ? 2 : 1;
   if (p.colt && p.T > 1) launches += 1;  // k2_rowleft
   info[1] = launches;
@@ -944,6 +1096,7 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   info[11] = p.units;
   info[12] = p.nbig;
   info[13] = p.S2;
+  info[14] = p.small ? 4 : p.carry;  // ih::Carry, 4 = K2s in-kernel carries
   return IH_OK;
 }
 

@@ -160,7 +160,9 @@ def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel
 
 PLAN_FIELDS = ("kernel", "launches", "segments", "segment_rows", "chunks_per_lane",
                "rows_per_batch", "warps_per_cta", "workspace_bytes", "column_tiles", "tile_width",
-               "resident_ctas", "ctas_per_segment", "big_segments", "tail_segment_rows")
+               "resident_ctas", "ctas_per_segment", "big_segments", "tail_segment_rows",
+               "carry")
+CARRIES = {0: "none", 1: "table", 2: "lookback", 3: "cluster", 4: "in_kernel"}
 
 
 def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "auto",
@@ -171,15 +173,19 @@ def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "au
                                                  _native.KERNELS[kernel], int(aligned16), info))
     d = dict(zip(PLAN_FIELDS, list(info)))
     d["kernel"] = {v: k for k, v in _native.KERNELS.items()}[d["kernel"]]
+    d["carry"] = CARRIES.get(d["carry"], str(d["carry"]))
     return d
 
 
 def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments: int,
-                  tail_pct: int = 0, tail_div: int = 0, cluster: bool = False) -> None:
+                  tail_pct: int = 0, tail_div: int = 0, cluster: bool = False,
+                  small: bool = False) -> None:
     """Pin the row-segment count (optional tail split, optional cluster/DSMEM
-    carries) for one problem shape; segments = 0 removes the pin."""
+    carries, or the K2s one-launch kernel with its own segmentation) for one
+    problem shape; segments = 0 removes the pin."""
+    flags = (1 if cluster else 0) | (2 if small else 0)
     _native.check(_native.lib().ih_plan_hint(frames, height, width, slab_bins, int(segments),
-                                             int(tail_pct), int(tail_div), 1 if cluster else 0))
+                                             int(tail_pct), int(tail_div), flags))
 
 
 _TUNED: dict = {}  # (frames, H, W, slab_bins) -> (segments, tail_pct, tail_div), this process

@@ -813,3 +813,50 @@ def test_to_host_private_pinned_released(monkeypatch):
     del v
     gc.collect()
     assert len(freed) == 1
+
+
+# ------------------------------------------------ K2s: one-launch small images
+def test_k2s_default_plan_and_cfg1(monkeypatch, golden_configs):
+    """One image with <= 4 bin groups plans the one-launch kernel by default;
+    BASELINE cfg1 (512x512x32, 8 groups: the count-table path by default)
+    through K2s reproduces the reference's golden crc."""
+    p = device.plan(1, 512, 512, 16)
+    assert (p["carry"], p["launches"]) == ("in_kernel", 1), p
+    assert device.plan(1, 512, 512, 32)["carry"] == "table"
+    px = O.synth_image(512, 512, 0)
+    lut16 = O.np_uniform_table(16)
+    assert np.array_equal(dev_compute(px, lut16, 16).cpu().numpy(), O.compute_crossweave(px, lut16, 16))
+    monkeypatch.setenv("IH_SMALL", "1")
+    assert device.plan(1, 512, 512, 32)["carry"] == "in_kernel"
+    got = dev_compute(px, O.np_uniform_table(32), 32).cpu().numpy()
+    assert crc_of(got) == golden_configs["512x512x32"]["crc"]
+
+
+def test_k2s_c1_instances(monkeypatch, golden_c1):
+    """All 200 acceptance-C1 instances through K2s (forced where it applies)."""
+    monkeypatch.setenv("IH_SMALL", "1")
+    for (w, h, b, tile, px), gold in zip(c1_images(200), golden_c1):
+        got = dev_compute(px, O.np_uniform_table(b), b).cpu().numpy()
+        assert crc_of(got) == gold["crc"], (w, h, b)
+
+
+@pytest.mark.parametrize("nseg", [0, 1, 2, 7, 40, 100000])
+def test_k2s_shapes_segments_slabs(monkeypatch, rng, nseg):
+    """K2s over widths 1..2048 (4 / 2 / 1 warp-groups, odd widths), heights up
+    to 1500, bins 1..256 with slabs and explicit LUTs, frame batches, and
+    forced segment counts from 1 to one row per segment."""
+    monkeypatch.setenv("IH_SMALL", "1")
+    if nseg:
+        monkeypatch.setenv("IH_NSEG", str(nseg))
+    for (F, h, w, bins) in [(1, 1, 1, 1), (1, 7, 3, 5), (2, 33, 127, 32), (1, 100, 129, 256),
+                            (3, 257, 513, 7), (1, 600, 1000, 64), (1, 1500, 2047, 3),
+                            (2, 64, 2048, 33), (1, 512, 512, 32)]:
+        lut = rng.integers(0, bins, 256).astype(np.uint8) if bins > 4 else O.np_uniform_table(bins)
+        lo = int(rng.integers(0, bins))
+        hi = int(rng.integers(lo + 1, bins + 1))
+        frames = rng.integers(0, 256, (F, h, w), dtype=np.uint8)
+        got = device.integral_histogram(device.upload_frames(frames), lut, bins,
+                                        bin_range=(lo, hi)).cpu().numpy()
+        for f in range(F):
+            want = O.compute_crossweave(frames[f], lut, bins)[lo:hi]
+            assert np.array_equal(got[f], want), (nseg, F, h, w, bins, lo, hi, f)
