@@ -194,6 +194,24 @@ int main() {
     snprintf(nm, sizeof nm, "k2like_cs_np1_nseg%d", nseg);
     timeit(nm, [&] { k2like<true, 1><<<dim3(nb, nseg, F), 480>>>(out, H, W, nb, S); });
   }
+  // occupancy-matched to k2_scan (2 CTAs of 15 warps per SM): a dummy dynamic
+  // shared-memory request of 100 KB per CTA
+  cudaFuncSetAttribute(k2like<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 << 10);
+  cudaFuncSetAttribute(k2like_planeorder<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 << 10);
+  cudaFuncSetAttribute(k2like_planeorder<4, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 << 10);
+  cudaFuncSetAttribute(k2like<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 << 10);
+  for (int nseg : {5, 9}) {
+    const int S = (H + nseg - 1) / nseg;
+    char nm[64];
+    snprintf(nm, sizeof nm, "occ2_k2like_cs_np4_nseg%d", nseg);
+    timeit(nm, [&] { k2like<true, 4><<<dim3(nb / 4, nseg, F), 480, 100 << 10>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "occ2_planeorder_rb2_nseg%d", nseg);
+    timeit(nm, [&] { k2like_planeorder<4, 2><<<dim3(nb / 4, nseg, F), 480, 100 << 10>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "occ2_planeorder_rb4_nseg%d", nseg);
+    timeit(nm, [&] { k2like_planeorder<4, 4><<<dim3(nb / 4, nseg, F), 480, 100 << 10>>>(out, H, W, nb, S); });
+    snprintf(nm, sizeof nm, "occ2_k2like_cs_np1_nseg%d", nseg);
+    timeit(nm, [&] { k2like<true, 1><<<dim3(nb, nseg, F), 480, 100 << 10>>>(out, H, W, nb, S); });
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   return 0;
