@@ -394,13 +394,15 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
             dist.barrier()
         torch.cuda.synchronize(dev)
 
-    # this rank's share: frames [f0, f1) x bins [b0, b1)
+    # this rank's share: frames [f0, f1) x bins [b0, b1); --share-of N times
+    # rank 0's share of an N-GPU run on this one GPU
+    pw = args.share_of if args.share_of else world
     if wl.shard == "frames":
-        f0, f1 = sharding.frame_shards(wl.frames, world)[rank]
+        f0, f1 = sharding.frame_shards(wl.frames, pw)[rank]
         b0, b1 = 0, wl.bins
     else:
         f0, f1 = 0, wl.frames
-        b0, b1 = sharding.bin_slabs(wl.bins, world)[rank]
+        b0, b1 = sharding.bin_slabs(wl.bins, pw)[rank]
     nloc, nb = f1 - f0, b1 - b0
     active = nloc > 0 and nb > 0
     host = np.stack([synth_image(wl.width, wl.height, k) for k in range(f0, max(f1, f0 + 1))])
@@ -592,6 +594,15 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     if traffic is None:
         line["roofline"]["traffic_note"] = ("no committed ncu capture of this workload with "
                                             "this launch plan (profiles/ncu_traffic.json)")
+    if args.share_of:
+        share_bytes = nloc * (wl.width * wl.height + 256 + 4 * nb * wl.width * wl.height)
+        line["metric"] = (METRIC + f" (projected {args.share_of}-GPU job: rank 0's share timed "
+                          "alone on this GPU)")
+        line["emulated_share"] = {
+            "of_gpus": args.share_of, "rank": 0, "frames": [f0, f1], "bins": [b0, b1],
+            "per_gpu_hbm_frac_step": share_bytes * args.steps / (total_ms / 1e3) / 1e9 / peak,
+            "note": "no other rank ran; the projection assumes every rank's share takes as long "
+                    "(equal shares, no inter-GPU traffic on the data path)"}
     if gather_ms is not None:
         line["gather_ms"] = gather_ms
     if queries is not None:
@@ -827,6 +838,9 @@ def main():
                     help="run each step's prepass and scan back to back on one stream")
     ap.add_argument("--ref-budget", type=float, default=10.0,
                     help="seconds of CPU work per reference sample (bounded)")
+    ap.add_argument("--share-of", type=int, default=0,
+                    help="time rank 0's share of an N-GPU run on this single GPU (per-GPU share "
+                         "evidence when only one GPU exists; not the job metric)")
     ap.add_argument("--csv", default="",
                     help="also append the run to this CSV (reference schema + roofline columns)")
     ap.add_argument("--dry-run", action="store_true",
@@ -852,6 +866,10 @@ def main():
     if launched and world != args.gpus:
         print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; they must agree",
               file=sys.stderr)
+        sys.exit(2)
+    if args.share_of and (world > 1 or args.share_of < 1 or wl.key == "512"):
+        print("bench.py: --share-of emulates one rank's share of a frame- or bin-sharded "
+              "workload on a single process", file=sys.stderr)
         sys.exit(2)
     if args.impl == "reference":
         run_reference(args, wl, rank, world)
