@@ -596,6 +596,7 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
                                             "this launch plan (profiles/ncu_traffic.json)")
     if args.share_of:
         share_bytes = nloc * (wl.width * wl.height + 256 + 4 * nb * wl.width * wl.height)
+        line["hbm_frac_step"] = share_bytes * args.steps / (total_ms / 1e3) / 1e9 / peak
         line["metric"] = (METRIC + f" (projected {args.share_of}-GPU job: rank 0's share timed "
                           "alone on this GPU)")
         line["emulated_share"] = {

@@ -80,6 +80,20 @@ def test_8k_256_single_gpu(img8k, golden_configs):
         plane = pinned.numpy().view(np.uint32)[None]
         expect = O.region_histograms(plane, regs[:2048])[:, 0]
         assert np.array_equal(got[:2048, b], expect), b
+    # every bin of the first 8,192 queries: the four corners of each query are
+    # gathered from the tensor by torch indexing (independent of K3) and
+    # combined with the oracle's inclusion-exclusion (core.py:184-194)
+    nq = 8192
+    rg = torch.from_numpy(regs[:nq].astype(np.int64)).to(t.device)
+    tv = t.view(torch.int32)
+    corner = []
+    for rr, cc in ((rg[:, 2], rg[:, 3]), (rg[:, 0] - 1, rg[:, 3]), (rg[:, 2], rg[:, 1] - 1),
+                   (rg[:, 0] - 1, rg[:, 1] - 1)):
+        ok = (rr >= 0) & (cc >= 0)
+        v = tv[:, rr.clamp(min=0), cc.clamp(min=0)].to(torch.int64) & 0xffffffff
+        corner.append((v * ok.to(torch.int64)).cpu().numpy())  # (256, nq)
+    expect_all = (corner[0] - corner[1] - corner[2] + corner[3]).T
+    assert np.array_equal(got[:nq].astype(np.int64), expect_all)
 
 
 def test_8k_256_eight_bin_shards(img8k, golden_configs):
