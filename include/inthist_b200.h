@@ -127,7 +127,11 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
  * a thread-block cluster (the <= 16 segments of a strip exchange their column
  * counts in distributed shared memory: one launch, no prepass; taken when the
  * plan allows it -- no column tiles, H < 65536); bit 1: the K2s one-launch
- * kernel (in-kernel carries; W <= 2048, 16-byte aligned rows, H < 65536).  Results are identical for
+ * kernel (in-kernel carries; W <= 2048, 16-byte aligned rows, H < 65536);
+ * bit 2: skewed segments -- tail_pct is then the percent of segments that
+ * are dispatched first and tail_div (> 100) their size ratio x 100 to the
+ * rest, so the older CTA of a co-resident pair (favoured by the warp
+ * scheduler) does proportionally more rows.  Results are identical for
  * every choice; only speed changes.  nseg = 0 removes the hint.  A small
  * process-wide table guarded by a mutex; device.autotune() fills it. */
 ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,

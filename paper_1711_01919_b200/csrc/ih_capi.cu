@@ -85,6 +85,8 @@ struct PlanHint {
 };
 constexpr int32_t kHintCluster = 1;  // ih_plan_hint flags: cluster (DSMEM) carries
 constexpr int32_t kHintSmall = 2;    // ih_plan_hint flags: K2s one-launch path
+constexpr int32_t kHintSkew = 4;     // ih_plan_hint flags: skewed segments (tail_pct = % of
+                                     // big segments, tail_div = size ratio x 100)
 constexpr int kMaxHints = 64;
 PlanHint g_hints[kMaxHints];
 int g_nhints = 0;
@@ -478,9 +480,37 @@ K2Plan plan_k2_uncached(int64_t frames, int64_t H, int64_t W, int nb, bool vec, 
   p.nseg = (int)((H + p.S - 1) / p.S);
   p.nbig = p.nseg;
   p.S2 = p.S;
+  // skewed segments (IH_SKEW_X100 / hint flag kHintSkew): the first ~pct %
+  // of the segments (dispatched first: the older CTA of each co-resident
+  // pair, which the warp scheduler favours) get rows in the ratio skew/100
+  // to the rest, so both CTAs of an SM finish together.  Measured on a
+  // one-wave 4K x 16-bin grid: lower-index CTAs end at ~73 us, the younger
+  // ones at ~90 us for equal work (profiles/r02e/tail_order.jsonl).
+  const bool skew_hint = (hinted_flags & kHintSkew) != 0;
+  const int64_t skew = env_int("IH_SKEW_X100", skew_hint ? hinted_tail_div : 0);
+  const int64_t skew_pct = env_int("IH_SKEW_PCT", skew_hint ? hinted_tail_pct : 50);
+  bool skewed = false;
+  if (skew > 100 && skew <= 400 && skew_pct > 0 && skew_pct < 100 && p.nseg >= 2 && H <= 65535) {
+    const int64_t n = p.nseg;
+    int64_t nbig = (n * skew_pct + 50) / 100;
+    if (nbig < 1) nbig = 1;
+    if (nbig >= n) nbig = n - 1;
+    // S * (nbig + (n - nbig) * 100 / skew) >= H
+    const double denom = (double)nbig + (double)(n - nbig) * 100.0 / (double)skew;
+    int64_t S = (int64_t)((double)H / denom) + 1;
+    int64_t S2 = S * 100 / skew;
+    if (S2 >= 1 && nbig * S < H && S < 65536) {
+      const int64_t rem = H - nbig * S;
+      p.S = (int)S;
+      p.nbig = (int)nbig;
+      p.S2 = (int)S2;
+      p.nseg = (int)(nbig + (rem + S2 - 1) / S2);
+      skewed = true;
+    }
+  }
   // tail split (IH_TAIL_PCT / hint): the last ~pct % of the rows become
   // segments of S/div rows, dispatched last (segment-major scan grid)
-  int64_t tail_pct = env_int("IH_TAIL_PCT", hinted_tail_pct);
+  int64_t tail_pct = skewed || skew_hint ? 0 : env_int("IH_TAIL_PCT", hinted_tail_pct);
   int64_t tail_div = env_int("IH_TAIL_DIV", hinted_tail_div > 0 ? hinted_tail_div : 4);
   if (tail_pct > 0 && tail_pct < 100 && tail_div > 1 && p.nseg > 1 && H <= 65535) {
     const int64_t s2 = (p.S + tail_div - 1) / tail_div;
@@ -510,6 +540,7 @@ K2Plan plan_k2_uncached(int64_t frames, int64_t H, int64_t W, int nb, bool vec, 
   // force it where it applies, IH_SMALL=0 disables it
   const int64_t small_env = env_int("IH_SMALL", -1);
   const bool auto_mode = hinted <= 0 && forced <= 0 && env_int("IH_TAIL_PCT", 0) == 0 &&
+                         env_int("IH_SKEW_X100", 0) == 0 &&
                          !want_cluster && env_int("IH_CARRY_LOOKBACK", 0) == 0 &&
                          env_int("IH_STAGED_STORES", 0) == 0 && env_int("IH_COLCOUNTS_SLAB", 0) == 0 &&
                          env_int("IH_MIN_SEG_ROWS", 0) == 0 && env_int("IH_TARGET_WAVES_X10", 0) == 0;

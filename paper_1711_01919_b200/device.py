@@ -179,11 +179,14 @@ def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "au
 
 def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments: int,
                   tail_pct: int = 0, tail_div: int = 0, cluster: bool = False,
-                  small: bool = False) -> None:
+                  small: bool = False, skew: bool = False) -> None:
     """Pin the row-segment count (optional tail split, optional cluster/DSMEM
     carries, or the K2s one-launch kernel with its own segmentation) for one
-    problem shape; segments = 0 removes the pin."""
-    flags = (1 if cluster else 0) | (2 if small else 0)
+    problem shape; segments = 0 removes the pin.  ``skew=True`` reads
+    (tail_pct, tail_div) as (percent of segments dispatched first, their size
+    ratio x 100 to the rest): skewed segments that let the older and the
+    younger CTA of an SM finish together."""
+    flags = (1 if cluster else 0) | (2 if small else 0) | (4 if skew else 0)
     _native.check(_native.lib().ih_plan_hint(frames, height, width, slab_bins, int(segments),
                                              int(tail_pct), int(tail_div), flags))
 
@@ -214,9 +217,11 @@ def load_tuning(path: str) -> int:
     name = torch.cuda.get_device_name(0) if torch.cuda.is_available() else "none"
     if doc.get("gpu") != name or doc.get("abi") != int(_native.lib().ih_abi_version()):
         return 0
-    for frames, height, width, nb, segs, tail_pct, tail_div in doc["hints"]:
-        set_plan_hint(frames, height, width, nb, segs, tail_pct, tail_div)
-        _TUNED[(frames, height, width, nb)] = (segs, tail_pct, tail_div)
+    for row in doc["hints"]:
+        frames, height, width, nb, segs, tail_pct, tail_div = row[:7]
+        flags = row[7] if len(row) > 7 else 0
+        set_plan_hint(frames, height, width, nb, segs, tail_pct, tail_div, skew=bool(flags & 4))
+        _TUNED[(frames, height, width, nb)] = (segs, tail_pct, tail_div, flags)
     return len(doc["hints"])
 
 
@@ -275,8 +280,8 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
     side = torch.cuda.Stream(dev)
     times = {}
 
-    def measure(n, tail_pct=0, tail_div=0):
-        set_plan_hint(frames, height, width, nb, n, tail_pct, tail_div)
+    def measure(n, tail_pct=0, tail_div=0, flags=0):
+        set_plan_hint(frames, height, width, nb, n, tail_pct, tail_div, skew=bool(flags & 4))
         need = workspace_bytes(frames, height, width, nb)
         w = ws if ws.numel() >= need else torch.empty(need, dtype=torch.uint8, device=dev)
         for _ in range(2):  # warm: attributes, caches
@@ -307,20 +312,27 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
 
     with torch.cuda.device(dev):
         for n in candidates:
-            times[(n, 0, 0)] = measure(n)
-        # second stage: short tail segments (run last) for the best count
+            times[(n, 0, 0, 0)] = measure(n)
+        # second stage for the best count: short tail segments (run last), and
+        # skewed segments (the first half, dispatched first, larger by 15-50 %)
         n0 = min(times, key=times.get)[0]
         if n0 > 1:
-            for tail_pct in (10, 20, 30):
-                set_plan_hint(frames, height, width, nb, n0, tail_pct, 4)
+            for tail_pct, tail_div, flags in ((10, 4, 0), (20, 4, 0), (30, 4, 0),
+                                              (50, 115, 4), (50, 130, 4), (50, 150, 4)):
+                set_plan_hint(frames, height, width, nb, n0, tail_pct, tail_div, skew=bool(flags))
                 p = plan(frames, height, width, nb)
                 if p["big_segments"] < p["segments"]:  # the split applies to this shape
-                    times[(n0, tail_pct, 4)] = measure(n0, tail_pct, 4)
+                    times[(n0, tail_pct, tail_div, flags)] = measure(n0, tail_pct, tail_div, flags)
     best = min(times, key=times.get)
-    set_plan_hint(frames, height, width, nb, *best)
+    set_plan_hint(frames, height, width, nb, *best[:3], skew=bool(best[3] & 4))
     _TUNED[(frames, height, width, nb)] = tuple(best)
+
+    def key(k):
+        if k[3] & 4:
+            return f"{k[0]}/s{k[2]}"
+        return f"{k[0]}" + (f"/t{k[1]}" if k[1] else "")
     return {"segments": best[0], "tail_pct": best[1], "tail_div": best[2],
-            "ms": {f"{k[0]}" + (f"/t{k[1]}" if k[1] else ""): round(v, 4) for k, v in times.items()}}
+            "skew": bool(best[3] & 4), "ms": {key(k): round(v, 4) for k, v in times.items()}}
 
 
 class GraphedIntegralHistogram:

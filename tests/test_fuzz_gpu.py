@@ -18,7 +18,8 @@ from paper_1711_01919_b200 import device  # noqa: E402
 KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY_CLUSTER",
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
          "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT",
-         "IH_STAGED_STORES", "IH_NO_RESTAGE", "IH_NO_ROWPACK", "IH_SMALL")
+         "IH_STAGED_STORES", "IH_NO_RESTAGE", "IH_NO_ROWPACK", "IH_SMALL", "IH_SKEW_X100",
+         "IH_SKEW_PCT")
 
 
 def _case(rng):
@@ -33,6 +34,9 @@ def _case(rng):
     if rng.random() < 0.3:
         env["IH_TAIL_PCT"] = str(int(rng.choice([10, 25, 50])))
         env["IH_TAIL_DIV"] = str(int(rng.choice([2, 4, 8])))
+    elif rng.random() < 0.3:  # skewed segments: first pct % larger by skew/100
+        env["IH_SKEW_X100"] = str(int(rng.choice([110, 130, 200])))
+        env["IH_SKEW_PCT"] = str(int(rng.choice([25, 50, 75])))
     carry = rng.choice(["table", "lookback", "cluster", "prefix", "small"])
     if carry == "small":  # K2s, where it applies (aligned rows, W <= 2048)
         env["IH_SMALL"] = "1"

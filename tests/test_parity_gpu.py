@@ -860,3 +860,22 @@ def test_k2s_shapes_segments_slabs(monkeypatch, rng, nseg):
         for f in range(F):
             want = O.compute_crossweave(frames[f], lut, bins)[lo:hi]
             assert np.array_equal(got[f], want), (nseg, F, h, w, bins, lo, hi, f)
+
+
+@pytest.mark.parametrize("skew,pct", [(115, 50), (130, 50), (150, 30), (300, 70)])
+def test_skewed_segments(monkeypatch, rng, skew, pct):
+    """Skewed segment sizes (the first pct % of the segments larger by skew/100,
+    IH_SKEW_X100 / the autotuner's hint flag) over column tiles, frame batches
+    and slabs: bit-exact, and the plan really is skewed."""
+    monkeypatch.setenv("IH_SKEW_X100", str(skew))
+    monkeypatch.setenv("IH_SKEW_PCT", str(pct))
+    for (F, h, w, bins, nseg) in [(1, 2160, 3840, 16, 37), (3, 300, 700, 12, 9), (2, 129, 2100, 5, 4)]:
+        monkeypatch.setenv("IH_NSEG", str(nseg))
+        p = device.plan(F, h, w, bins)
+        assert p["big_segments"] < p["segments"] and p["segment_rows"] > p["tail_segment_rows"], p
+        frames = rng.integers(0, 256, (F, h, w), dtype=np.uint8)
+        lut = O.np_uniform_table(bins)
+        got = device.integral_histogram(device.upload_frames(frames), lut, bins).cpu().numpy()
+        for f in range(F):
+            assert np.array_equal(got[f], O.compute_crossweave(frames[f], lut, bins)), (F, h, w, bins, f)
+
