@@ -212,6 +212,36 @@ int main() {
     snprintf(nm, sizeof nm, "occ2_k2like_cs_np1_nseg%d", nseg);
     timeit(nm, [&] { k2like<true, 1><<<dim3(nb, nseg, F), 480, 100 << 10>>>(out, H, W, nb, S); });
   }
+  // cfg1 shape (512 x 512 x 32 bins, one frame, 33.5 MB): pure stores with
+  // the K2 pattern, timed as 20 back-to-back launches rotating over 8 output
+  // buffers (268 MB > L2, like bench.py --workload 512) and over one buffer
+  // (L2-resident, like scripts/graph_time.py)
+  {
+    const int h = 512, w = 512, b = 32;
+    const size_t one = (size_t)b * h * w;
+    for (int nbuf : {1, 8}) {
+      for (int nseg : {8, 16, 32, 64}) {
+        const int S = (h + nseg - 1) / nseg;
+        const int wpc = w / 128;  // warps per CTA
+        cudaEventRecord(e0);
+        for (int i = 0; i < 20; ++i)
+          k2like<true, 4><<<dim3(b / 4, nseg, 1), wpc * 32>>>(out + (i % nbuf) * one, h, w, b, S);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        float ms;
+        cudaEventElapsedTime(&ms, e0, e1);
+        printf("{\"probe\": \"cfg1_k2like_np4_nseg%d_bufs%d\", \"us_per_launch\": %.2f, \"gbs\": %.1f}\n",
+               nseg, nbuf, ms * 1000 / 20, one * 4 * 20 / ms / 1e6);
+      }
+    }
+    cudaEventRecord(e0);
+    for (int i = 0; i < 20; ++i) cudaMemsetAsync(out + (i % 8) * one, 0, one * 4);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    printf("{\"probe\": \"cfg1_memset_bufs8\", \"us_per_launch\": %.2f}\n", ms * 1000 / 20);
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   return 0;

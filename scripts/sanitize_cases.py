@@ -15,12 +15,14 @@ envs = [{}, {"IH_NSEG": "3"}, {"IH_NSEG": "5", "IH_TABLE_SUM_MAX": "1"},
         {"IH_NSEG": "4", "IH_CARRY_LOOKBACK": "1"}, {"IH_NO_TMA": "1", "IH_NSEG": "2"},
         {"IH_ROWS_PER_BATCH": "1", "IH_NSEG": "3"}, {"IH_NSEG": "6", "IH_COLCOUNTS_SLAB": "1"},
         {"IH_NSEG": "3", "IH_NO_COLTILE": "1"}, {"IH_NSEG": "4", "IH_TAIL_PCT": "30"},
-        {"IH_NSEG": "3", "IH_CARRY_CLUSTER": "1"}, {"IH_NSEG": "2", "IH_STAGED_STORES": "1"}]
+        {"IH_NSEG": "3", "IH_CARRY_CLUSTER": "1"}, {"IH_NSEG": "2", "IH_STAGED_STORES": "1"},
+        {"IH_SMALL": "1"}, {"IH_SMALL": "1", "IH_NSEG": "7"},
+        {"IH_NSEG": "5", "IH_SKEW_X100": "130"}]
 bad = 0
 for env in envs:
     for k in ("IH_NSEG", "IH_TABLE_SUM_MAX", "IH_CARRY_LOOKBACK", "IH_NO_TMA", "IH_ROWS_PER_BATCH",
               "IH_COLCOUNTS_SLAB", "IH_NO_COLTILE", "IH_TAIL_PCT", "IH_CARRY_CLUSTER",
-              "IH_STAGED_STORES"):
+              "IH_STAGED_STORES", "IH_SMALL", "IH_SKEW_X100"):
         os.environ.pop(k, None)
     os.environ.update(env)
     for (h, w, b) in cases:
@@ -61,4 +63,8 @@ for shape, dt in (((33, 260), np.uint8), ((33, 259), np.uint8), ((17, 64), np.ui
 for dt in (np.uint8, np.uint16, np.uint32, np.float64, np.complex128):
     a = (rng.random((37, 45)) * 100).astype(dt)
     bad += not np.array_equal(S.transpose(a), a.T)
+# K7: the wavefront with a recorded trace
+pxw = rng.integers(0, 256, (50, 70), dtype=np.uint8)
+cw, ev = device.wavefront(device.upload_image(pxw), O.np_uniform_table(5), 5, 16)
+bad += not np.array_equal(cw.cpu().numpy(), O.compute_crossweave(pxw, O.np_uniform_table(5), 5))
 print("sanitize cases done, mismatches:", bad)
