@@ -164,3 +164,62 @@ def test_plan_variants_on_cpu(monkeypatch):
         device.set_plan_hint(4, 1000, 700, 9, 6, 120, 4)
     with pytest.raises(PE):
         device.set_plan_hint(4, 1000, 700, 9, -1)
+
+
+def test_plan_cache_follows_knobs_and_hints(monkeypatch):
+    """Plans are cached per (IH_* fingerprint, hint generation, shape): a knob
+    or hint change between calls takes effect on the next call."""
+    from paper_1711_01919_b200 import device
+
+    base = device.plan(8, 1080, 1920, 32)["segments"]
+    monkeypatch.setenv("IH_NSEG", "7")
+    assert device.plan(8, 1080, 1920, 32)["segments"] == 7
+    monkeypatch.setenv("IH_NSEG", "11")
+    assert device.plan(8, 1080, 1920, 32)["segments"] == 11
+    monkeypatch.delenv("IH_NSEG")
+    assert device.plan(8, 1080, 1920, 32)["segments"] == base
+    device.set_plan_hint(8, 1080, 1920, 32, 5)
+    try:
+        assert device.plan(8, 1080, 1920, 32)["segments"] == 5
+    finally:
+        device.set_plan_hint(8, 1080, 1920, 32, 0)
+    assert device.plan(8, 1080, 1920, 32)["segments"] == base
+
+
+def test_skewed_segment_plans(monkeypatch):
+    """Skewed segments: the first pct % of the segments are larger by
+    skew/100, the plan still covers every row, and the hint flag form equals
+    the environment form."""
+    from paper_1711_01919_b200 import device
+
+    monkeypatch.setenv("IH_NSEG", "37")
+    monkeypatch.setenv("IH_SKEW_X100", "125")
+    p = device.plan(1, 2160, 3840, 16)
+    S, nbig, S2, n = p["segment_rows"], p["big_segments"], p["tail_segment_rows"], p["segments"]
+    assert nbig == 19 and S2 == S * 100 // 125 and nbig * S + (n - nbig - 1) * S2 < 2160 <= nbig * S + (n - nbig) * S2
+    monkeypatch.delenv("IH_SKEW_X100")
+    monkeypatch.delenv("IH_NSEG")
+    device.set_plan_hint(1, 2160, 3840, 16, 37, 50, 125, skew=True)
+    try:
+        q = device.plan(1, 2160, 3840, 16)
+        assert (q["segment_rows"], q["big_segments"], q["tail_segment_rows"], q["segments"]) == (S, nbig, S2, n)
+    finally:
+        device.set_plan_hint(1, 2160, 3840, 16, 0)
+
+
+def test_k2s_plans(monkeypatch):
+    """The one-launch small-image kernel: planned for <= 4 bin groups of one
+    small frame, forced by IH_SMALL=1, off with IH_SMALL=0, never for column
+    tiles or unaligned rows; its workspace holds the flags and aggregates."""
+    from paper_1711_01919_b200 import device
+
+    p = device.plan(1, 512, 512, 16)
+    assert (p["carry"], p["launches"]) == ("in_kernel", 1)
+    assert p["workspace_bytes"] > 0
+    assert device.plan(1, 512, 512, 32)["carry"] == "table"
+    assert device.plan(1, 512, 512, 16, aligned16=False)["carry"] != "in_kernel"
+    assert device.plan(1, 512, 4096, 4)["carry"] != "in_kernel"
+    monkeypatch.setenv("IH_SMALL", "1")
+    assert device.plan(1, 512, 512, 32)["carry"] == "in_kernel"
+    monkeypatch.setenv("IH_SMALL", "0")
+    assert device.plan(1, 512, 512, 16)["carry"] != "in_kernel"

@@ -92,3 +92,34 @@ def test_reference_arm_reports_n_gpus():
     d = json.loads(r.stdout.strip().splitlines()[-1])
     assert d["n_gpus"] == 2 and d["impl"] == "reference"
     assert d["config"]["key"] == "512" and "host_cpu" in d["config"]
+
+
+def test_share_of_is_single_process_only():
+    """--share-of N emulates rank 0's share of an N-GPU run on one process;
+    it is refused under a multi-rank launch and for the replica workload."""
+    r = _bench("--share-of", "4", "--workload", "512", "--steps", "3", "--warmup", "3")
+    assert r.returncode == 2 and "share-of" in r.stderr
+    e = dict(os.environ, RANK="0", LOCAL_RANK="0", WORLD_SIZE="2")
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                        "--share-of", "4", "--steps", "3", "--warmup", "3"],
+                       capture_output=True, text=True, env=e, timeout=300)
+    assert r.returncode == 2 and "share-of" in r.stderr
+
+
+def test_csv_row_schema(tmp_path):
+    """--csv appends the reference's CSV columns plus the roofline columns."""
+    sys.path.insert(0, ROOT)
+    import bench
+
+    line = {"value": 100.0, "steps": 5, "n_gpus": 1, "parity": "output crc32 == reference golden",
+            "hbm_frac_step": 0.5, "roofline": {"traffic": 2.0e8},
+            "config": {"histograms_per_step": 1, "host_cpu": "cpu model (4 threads)"}}
+    path = tmp_path / "b.csv"
+    bench.write_csv(str(path), line, bench.WORKLOADS["512"])
+    bench.write_csv(str(path), line, bench.WORKLOADS["512"])
+    rows = path.read_text().splitlines()
+    from paper_1711_01919_b200.harness import CSV_HEADER
+    assert rows[0] == CSV_HEADER + "," + bench.CSV_EXTRA and len(rows) == 3
+    cols = rows[1].split(",")
+    assert cols[0] == "single_pass" and cols[1:4] == ["512", "512", "32"] and cols[10] == "53891c64"
+    assert cols[11] == "1" and cols[15] == "200000000"
