@@ -771,6 +771,16 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
                        ? (uint32_t*)((uint8_t*)ws + k2_table_bytes(c.frames, p) +
                                      k2_rowleft_bytes(c.frames, c.H, p))
                        : nullptr;
+  if (p.nbp <= ih::kGroup && !p.colt && env_int("IH_COLCOUNTS_G1", 1) != 0 &&
+      !knobs().colcounts_slab) {  // one group of <= 4 bins: counts in registers
+    dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
+    auto kern = al ? ih::k2_colcounts_g1<true> : ih::k2_colcounts_g1<false>;
+    if (launch(kern, grid, dim3(256), 0, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch, c.fstride,
+               c.lut, segs(p), p.nseg, p.nbp, p.Wp, (uint16_t*)ws) != cudaSuccess)
+      return cuda_fail("k2_colcounts_g1");
+    ++c.launched;
+    return launch_colprefix(c, ws);
+  }
   if (!knobs().colcounts_slab) {  // all bins in one pass (shared atomics)
     dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
     auto kern = al ? ih::k2_colcounts_all<true> : ih::k2_colcounts_all<false>;

@@ -238,6 +238,98 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
 }
 
 // ---------------------------------------------------------------------------
+// k2_colcounts_g1: the same table for slabs of ONE packed group (<= 4 bins,
+// e.g. B = 1 / 2 / 4): counting in registers instead of shared atomics.  A
+// lane's 4 columns take one one-hot word per pixel (the scan's packed-byte
+// table: one byte per bin of the group), added byte-wise into 4 registers and
+// widened into 16-bit lanes every 255 rows; the 8 warps' column counts are
+// summed through shared memory and dumped as the u16 table rows of the slab's
+// <= 4 bins.  Same grid and output as k2_colcounts_all (no column tiles).
+// ---------------------------------------------------------------------------
+template <bool ALIGNED>
+__global__ void __launch_bounds__(256) k2_colcounts_g1(
+    const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
+    RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws) {
+  __shared__ uint32_t oh[kOneHotEntries];
+  __shared__ uint4 part[8][2][32];  // [warp][bins 0/2 | 1/3][lane] 16-bit lanes, 4 columns
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int64_t c = (int64_t)blockIdx.x * kChunk + 4 * lane;
+  const int s = blockIdx.y;
+  const int64_t f = blockIdx.z;
+  griddep_launch_dependents();
+  build_onehot(oh, lut, 0);
+  uint32_t inval[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) inval[k] = (c + k < W) ? 0u : 256u;
+  __syncthreads();
+  const int64_t seg0 = sg.start(s);
+  const int64_t seg1 = min(sg.start(s + 1), H);
+  uint32_t ce[4] = {0u, 0u, 0u, 0u}, co[4] = {0u, 0u, 0u, 0u};
+  if (c < W) {
+    // this warp's rows: seg0 + warp + 8 i (32-bit counters: segments are
+    // < 65536 rows), pointer-stepped, predicates only on the last < 8 rows
+    const int nrows = (int)(seg1 - seg0);
+    int left = nrows > warp ? (nrows - warp + 7) / 8 : 0;
+    const uint8_t* q = img + f * fstride + (seg0 + warp) * pitch + c;
+    const int64_t rstep = 8 * pitch;
+    auto load_px = [&](const uint8_t* row) -> uint32_t {
+      if (ALIGNED) return __ldg(reinterpret_cast<const uint32_t*>(row));
+      uint32_t px = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (c + k < W) px |= (uint32_t)__ldg(row + k) << (8 * k);
+      return px;
+    };
+    auto add4 = [&](uint32_t px, uint32_t acc[4]) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) acc[k] += oh[((px >> (8 * k)) & 0xffu) | inval[k]];
+    };
+    constexpr int U = 8;
+    while (left > 0) {
+      // byte-packed counts: <= 248 rows (31 x 8) per flush into 16-bit lanes
+      const int chunk = left < 248 ? left : 248;
+      uint32_t acc[4] = {0u, 0u, 0u, 0u};
+      for (int it = 0; it < chunk / U; ++it) {
+        uint32_t px[U];
+#pragma unroll
+        for (int i = 0; i < U; ++i) px[i] = load_px(q + i * rstep);
+#pragma unroll
+        for (int i = 0; i < U; ++i) add4(px[i], acc);
+        q += U * rstep;
+      }
+      for (int i = 0; i < chunk % U; ++i, q += rstep) add4(load_px(q), acc);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ce[k] += acc[k] & 0x00ff00ffu;
+        co[k] += (acc[k] >> 8) & 0x00ff00ffu;
+      }
+      left -= chunk;
+    }
+  }
+  part[warp][0][lane] = make_uint4(ce[0], ce[1], ce[2], ce[3]);
+  part[warp][1][lane] = make_uint4(co[0], co[1], co[2], co[3]);
+  __syncthreads();
+  griddep_wait();  // PDL: complete only after the predecessor (transitivity)
+  if (warp < 2) {  // warp 0: bins 0/2, warp 1: bins 1/3
+    uint4 t = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      const uint4 x = part[w][warp][lane];
+      t.x += x.x; t.y += x.y; t.z += x.z; t.w += x.w;
+    }
+    uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp) * Wp + (int64_t)blockIdx.x * kChunk + 4 * lane;
+    // 16-bit lanes: low half = bin `warp`, high half = bin `warp + 2`
+    if (warp < nbp)
+      *reinterpret_cast<uint2*>(dst + (int64_t)warp * Wp) =
+          make_uint2(__byte_perm(t.x, t.y, 0x5410), __byte_perm(t.z, t.w, 0x5410));
+    if (warp + 2 < nbp)
+      *reinterpret_cast<uint2*>(dst + (int64_t)(warp + 2) * Wp) =
+          make_uint2(__byte_perm(t.x, t.y, 0x7632), __byte_perm(t.z, t.w, 0x7632));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k2_colprefix: in place, ws[f][s][b][c] <- sum_{s' < s} counts[f][s'][b][c]
 // (u16; only used when H <= 65535 so every prefix fits).  Thread per
 // (f, b, 4 columns); loads are issued 8 segments at a time before any store.

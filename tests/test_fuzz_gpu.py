@@ -19,7 +19,7 @@ KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
          "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT",
          "IH_STAGED_STORES", "IH_NO_RESTAGE", "IH_NO_ROWPACK", "IH_SMALL", "IH_SKEW_X100",
-         "IH_SKEW_PCT")
+         "IH_SKEW_PCT", "IH_COLCOUNTS_G1")
 
 
 def _case(rng):
@@ -47,6 +47,8 @@ def _case(rng):
     elif carry == "prefix":
         env["IH_TABLE_SUM_MAX"] = "1"
     env["IH_ROWS_PER_BATCH"] = str(int(rng.choice([1, 2, 4])))
+    if rng.random() < 0.3:
+        env["IH_COLCOUNTS_G1"] = "0"  # <= 4-bin slabs: the shared-atomic count kernel
     for k, p in (("IH_NO_TMA", 0.2), ("IH_NO_COLTILE", 0.2), ("IH_COLCOUNTS_SLAB", 0.2),
                  ("IH_NO_PDL", 0.2), ("IH_STAGED_STORES", 0.25)):
         if rng.random() < p:
