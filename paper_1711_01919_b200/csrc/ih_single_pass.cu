@@ -207,20 +207,21 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
   };
   if (c < W) {
     // rows seg0 + warp + i*nw; 8 rows of loads in flight per warp, addressed
-    // by stepping one row pointer (no 64-bit multiply per load)
+    // by stepping one row pointer (no 64-bit multiply per load); a 32-bit row
+    // count (segments are < 65536 rows) and predicates only on the last < 8
     constexpr int U = 8;
     const int64_t rstep = (int64_t)nw * pitch;
-    const int64_t step = (int64_t)nw * U;
+    const int nrows = (int)(seg1 - seg0);
+    const int mine = nrows > warp ? (nrows - warp + nw - 1) / nw : 0;
     const uint8_t* p = base + (seg0 + warp) * pitch + c;
-    for (int64_t r = seg0 + warp; r < seg1; r += step, p += U * rstep) {
+    for (int it = 0; it < mine / U; ++it, p += U * rstep) {
       uint32_t px[U];
-      const uint8_t* q = p;
 #pragma unroll
-      for (int i = 0; i < U; ++i, q += rstep) px[i] = r + i * nw < seg1 ? load_px(q) : 0u;
+      for (int i = 0; i < U; ++i) px[i] = load_px(p + i * rstep);
 #pragma unroll
-      for (int i = 0; i < U; ++i)
-        if (r + i * nw < seg1) count4(px[i]);
+      for (int i = 0; i < U; ++i) count4(px[i]);
     }
+    for (int i = 0; i < mine % U; ++i, p += rstep) count4(load_px(p));
   }
   __syncthreads();
   griddep_wait();  // PDL: complete only after the predecessor (transitivity)
