@@ -212,6 +212,31 @@ int main() {
     snprintf(nm, sizeof nm, "occ2_k2like_cs_np1_nseg%d", nseg);
     timeit(nm, [&] { k2like<true, 1><<<dim3(nb, nseg, F), 480, 100 << 10>>>(out, H, W, nb, S); });
   }
+  // lone CTAs: one 480-thread CTA per SM (148 CTAs, a 100 KB dummy smem request
+  // keeps a second one off the SM) writing K2's store pattern: the per-SM
+  // store rate a single k2_scan CTA could reach if it did nothing else
+  {
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    cudaFuncSetAttribute(k2like<true, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    for (int smem_kb : {200, 100}) {  // 200 KB: one CTA per SM; 100 KB: two
+      const int nseg = (sms + 7) / 8;  // 8 groups x nseg segments ~ one CTA per SM
+      const int S = (H + nseg - 1) / nseg;
+      char nm[64];
+      snprintf(nm, sizeof nm, "lone_k2like_np4_smem%dKB_ctas%d", smem_kb, 8 * nseg);
+      timeit(nm, [&] { k2like<true, 4><<<dim3(nb / 4, nseg, 1), 480, (size_t)smem_kb << 10>>>(out, H, W, nb, S); });
+    }
+    // the same lone CTAs with 32-byte stores (240 threads: 8 columns per lane)
+    // and with whole-row TMA bulk stores staged in shared memory
+    const int nseg = (sms + 7) / 8;
+    const int S = (H + nseg - 1) / nseg;
+    cudaFuncSetAttribute(k2like_v8<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    timeit("lone_k2like_v8_np4", [&] { k2like_v8<4><<<dim3(nb / 4, nseg, 1), 256, 200 << 10>>>(out, H, W, nb, S); });
+    cudaFuncSetAttribute(k2like_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 << 10);
+    timeit("lone_k2like_tma_np4", [&] { k2like_tma<4><<<dim3(nb / 4, nseg, 1), 480, 200 << 10>>>(out, H, W, nb, S); });
+    const double lone_bytes = (double)nb * H * W * 4;
+    printf("{\"note\": \"lone_* lines write one frame (%.0f MB): GB/s = that / ms; the gbs field assumes the whole buffer\"}\n", lone_bytes / 1e6);
+  }
   // cfg1 shape (512 x 512 x 32 bins, one frame, 33.5 MB): pure stores with
   // the K2 pattern, timed as 20 back-to-back launches rotating over 8 output
   // buffers (268 MB > L2, like bench.py --workload 512) and over one buffer
