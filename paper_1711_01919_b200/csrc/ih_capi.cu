@@ -454,6 +454,22 @@ K2Plan plan_k2_uncached(int64_t frames, int64_t H, int64_t W, int nb, bool vec, 
       }
     }
     nseg = best;
+  } else if (raw <= (double)max_seg && !many && env_int("IH_FEW_UNITS_V1", 0) == 0) {
+    // few frames x groups, several CTAs per SM: the fewest segments (>= raw/2,
+    // i.e. >= about one wave) whose last wave is >= 95 % full -- every extra
+    // segment costs a prologue and a carry slot, and a partly filled last
+    // wave leaves its slots idle (round 2 sweep, profiles/r02h/: HD x 4
+    // 19 -> 9 segments 0.735 -> 0.867 of HBM, 512^2 x 8 frames 40 -> 20)
+    const int64_t lo = (int64_t)(raw / 2) > 1 ? (int64_t)(raw / 2) : 1;
+    nseg = (int64_t)(raw + 0.5);
+    for (int64_t n = lo; n <= max_seg && n <= (int64_t)(2 * raw) + 1; ++n) {
+      const double w = (double)(units * n) / (double)slots;
+      const double full = w / (double)(int64_t)(w + 0.999999);
+      if (full >= 0.95) {
+        nseg = n;
+        break;
+      }
+    }
   } else if (raw <= (double)max_seg) {
     nseg = many ? (int64_t)(raw + 0.999) : (int64_t)(raw + 0.5);
   } else {
