@@ -344,6 +344,7 @@ __device__ __forceinline__ uint2 add_u16x4(uint2 a, uint2 b) {  // lanes never c
 // run totals are exclusive-scanned with 3 shuffles inside the 8-lane group, so
 // every load is issued up front (no chain of round trips over the segments).
 constexpr int kPrefixLanes = 8;
+constexpr int kPrefixRegs = 8;  // slots per lane held in registers (nseg <= 64)
 
 __global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, int64_t frames,
                                                      int nseg, int nbp, int64_t Wp) {
@@ -362,6 +363,33 @@ __global__ void __launch_bounds__(256) k2_colprefix(uint16_t* __restrict__ ws, i
     if (__all_sync(kFull, !live)) break;
     const int64_t f = live ? gi / quads : 0, q = live ? gi % quads : 0;
     uint2* p = reinterpret_cast<uint2*>(ws + f * nseg * plane) + q;
+    if (per <= kPrefixRegs) {  // <= 64 segments: every load of the run in flight at once
+      uint2 v[kPrefixRegs];
+      uint2 tot = make_uint2(0u, 0u);
+#pragma unroll
+      for (int i = 0; i < kPrefixRegs; ++i) {
+        const int j = j0 + i;
+        v[i] = live && j < j1 && j < nseg - 1 ? p[(int64_t)j * quads] : make_uint2(0u, 0u);
+        tot = add_u16x4(tot, v[i]);
+      }
+      uint2 inc = tot;
+#pragma unroll
+      for (int d = 1; d < kPrefixLanes; d <<= 1) {
+        const uint32_t x = __shfl_up_sync(kFull, inc.x, d, kPrefixLanes);
+        const uint32_t y = __shfl_up_sync(kFull, inc.y, d, kPrefixLanes);
+        if (sub >= d) inc = add_u16x4(inc, make_uint2(x, y));
+      }
+      uint2 run = make_uint2(inc.x - tot.x, inc.y - tot.y);
+#pragma unroll
+      for (int i = 0; i < kPrefixRegs; ++i) {
+        const int j = j0 + i;
+        if (live && j < j1) {
+          p[(int64_t)j * quads] = run;
+          run = add_u16x4(run, v[i]);
+        }
+      }
+      continue;
+    }
     uint2 tot = make_uint2(0u, 0u);
     for (int j = j0; j < j1 && j < nseg - 1; ++j)
       if (live) tot = add_u16x4(tot, p[(int64_t)j * quads]);
