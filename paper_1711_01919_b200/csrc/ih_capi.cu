@@ -1198,6 +1198,19 @@ ih_status ih_likelihood_map_ws(const uint32_t* t, int32_t nb, int64_t height, in
           tpl, nb, (int64_t)h * w, M);
     if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k5_metric_table");
     const int64_t P = env_int("IH_K5_PAIRS", 2);  // placements per thread (32 apart)
+    // output rows h apart per thread (2: HD x32 64x64 0.1003 -> 0.0992 ms,
+    // 8x8 0.1068 -> 0.0981; 4 / 8 spill: profiles/r02h/k5_chain.jsonl)
+    const int64_t KC = env_int("IH_K5_CHAIN", 2);
+    if ((KC == 2 || KC == 4 || KC == 8) && (P == 2 || P == 4)) {
+      const int64_t nchains = (R + (int64_t)h * KC - 1) / ((int64_t)h * KC) * h;
+      dim3 grid((unsigned)((C + 256 * P - 1) / (256 * P)), (unsigned)(nchains < 65535 ? nchains : 65535));
+      auto k = KC == 2 ? (P == 4 ? ih::k5_likelihood_map_chain<2, 4> : ih::k5_likelihood_map_chain<2, 2>)
+             : KC == 4 ? (P == 4 ? ih::k5_likelihood_map_chain<4, 4> : ih::k5_likelihood_map_chain<4, 2>)
+                       : ih::k5_likelihood_map_chain<8, 2>;  // (K = 8 only with P = 2)
+      k<<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h, w, M, out);
+      if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k5_likelihood_map_chain");
+      return IH_OK;
+    }
     if (P == 2 || P == 4) {
       dim3 grid((unsigned)((C + 256 * P - 1) / (256 * P)), (unsigned)(R < 65535 ? R : 65535));
       // bins per step (P = 2): 2 -> 48 registers, the best occupancy / MLP

@@ -466,4 +466,71 @@ __global__ void __launch_bounds__(256) k5_likelihood_map_tabp(const uint32_t* __
   }
 }
 
+// K5 (table) over chains of output rows h apart: output row r reads tensor
+// rows r - 1 and r + h - 1, so rows r and r + h share row r + h - 1.  A
+// thread takes K output rows i0 + h*k (k < K) of P placements (32 apart, as
+// _tabp) and, per bin, the horizontal differences
+//     D_k = T(row_k, j + w - 1) - T(row_k, j - 1),  row_k = i0 - 1 + h*k
+// of K + 1 tensor rows (2 loads each); window count n_k = D_{k+1} - D_k
+// (exact in u32).  2P(K+1) corner loads per bin instead of 4PK.  Same terms,
+// same bin order: bit-identical to _tabp.
+template <int K, int P>
+__global__ void __launch_bounds__(256) k5_likelihood_map_chain(const uint32_t* __restrict__ t,
+                                                                int nb, int64_t H, int64_t W,
+                                                                int h, int w,
+                                                                const double* __restrict__ M,
+                                                                double* __restrict__ out) {
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const int64_t n1 = (int64_t)h * w + 1;
+  const int64_t plane = H * W;
+  const int64_t blocks_per_i0 = (R + (int64_t)h * K - 1) / ((int64_t)h * K);
+  const int64_t nchains = blocks_per_i0 * h;
+  for (int64_t y = blockIdx.y; y < nchains; y += gridDim.y) {
+    const int64_t i0 = (y % h) + (int64_t)h * K * (y / h);  // first output row of the chain
+    if (i0 >= R) continue;
+    const int64_t g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t j = (g >> 5) * (32 * P) + (g & 31);
+    if (j >= C) continue;
+    bool ok[P];
+#pragma unroll
+    for (int q = 0; q < P; ++q) ok[q] = j + 32 * q < C;
+    int nrows = 0;  // valid output rows of this chain
+#pragma unroll
+    for (int k = 0; k < K; ++k) nrows += i0 + (int64_t)h * k < R;
+    double acc[K][P];
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int q = 0; q < P; ++q) acc[k][q] = 0.0;
+    const double* Mb = M;
+    for (int b = 0; b < nb; ++b, Mb += n1) {
+      const uint32_t* p = t + (int64_t)b * plane;
+      uint32_t D[K + 1][P];
+#pragma unroll
+      for (int k = 0; k <= K; ++k) {
+        const int64_t row = i0 - 1 + (int64_t)h * k;
+        const bool rv = row >= 0 && k <= nrows;  // row K only if it bounds a valid output
+        const uint32_t* pr = p + row * W;
+#pragma unroll
+        for (int q = 0; q < P; ++q) {
+          const int64_t jj = j + 32 * q;
+          const uint32_t right = rv && ok[q] ? __ldg(pr + jj + w - 1) : 0u;
+          const uint32_t left = rv && ok[q] && jj > 0 ? __ldg(pr + jj - 1) : 0u;
+          D[k][q] = right - left;
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < K; ++k)
+#pragma unroll
+        for (int q = 0; q < P; ++q)
+          if (k < nrows && ok[q]) acc[k][q] += __ldg(Mb + (D[k + 1][q] - D[k][q]));
+    }
+#pragma unroll
+    for (int k = 0; k < K; ++k)
+#pragma unroll
+      for (int q = 0; q < P; ++q)
+        if (k < nrows && ok[q]) out[(i0 + (int64_t)h * k) * C + j + 32 * q] = fmin(fmax(acc[k][q], 0.0), 1.0);
+  }
+}
+
 }  // namespace ih

@@ -19,7 +19,7 @@ KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
          "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT",
          "IH_STAGED_STORES", "IH_NO_RESTAGE", "IH_NO_ROWPACK", "IH_SMALL", "IH_SKEW_X100",
-         "IH_SKEW_PCT", "IH_COLCOUNTS_G1")
+         "IH_SKEW_PCT", "IH_COLCOUNTS_G1", "IH_K5_CHAIN")
 
 
 def _case(rng):
@@ -140,7 +140,13 @@ def test_fuzz_queries(monkeypatch, seed):
         tmpl /= tmpl.sum()
         for metric in ("intersection", "bhattacharyya"):
             ref = O.np_likelihood_map(full, tmpl, h, w, metric)
-            for direct in ("0", "1"):
+            base = None
+            for direct, chain in (("0", "2"), ("0", "0"), ("0", "4"), ("1", "0")):
                 monkeypatch.setenv("IH_K5_DIRECT", direct)
+                monkeypatch.setenv("IH_K5_CHAIN", chain)
                 got = device.likelihood_map(t, tmpl, h, w, metric).cpu().numpy()
-                assert np.abs(got - ref).max() < 1e-12, (H, W, h, w, metric, direct)
+                assert np.abs(got - ref).max() < 1e-12, (H, W, h, w, metric, direct, chain)
+                if base is None:
+                    base = got
+                else:  # every K5 variant computes the same terms in the same order
+                    assert np.array_equal(got, base), (H, W, h, w, metric, direct, chain)
