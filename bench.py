@@ -118,7 +118,9 @@ def committed_traffic(wl: Workload, plan: dict):
     # captured per segment count without tail split or skew: both only move
     # rows between segments, so the DRAM bytes of the same count are the same
     # (the reads are the image plus one carry table per segment)
-    cap = e.get("by_segments", {}).get(str(plan.get("segments")))
+    # (keys "<n>/kb2": the bin-pair grouping, two bins per scan CTA)
+    key = str(plan.get("segments")) + ("/kb2" if plan.get("bins_per_cta") == 2 else "")
+    cap = e.get("by_segments", {}).get(key)
     return cap["bytes"] if cap else None
 
 

@@ -115,7 +115,8 @@ ih_status ih_ih_scan(const uint8_t *img, int64_t frames, int64_t height, int64_t
  *   info[12] big segments (the rest are tail segments)  info[13] tail segment rows
  *   info[14] segment carries: 0 none, 1 count table (prepass kernels), 2 look-back,
  *            3 cluster (DSMEM), 4 in-kernel (K2s: one launch, small images)
- * (`info` holds 15 entries.)  Same shape/parameter errors as ih_integral_histogram. */
+ *   info[15] bins per scan CTA (1, 2: rows packed into the spare bytes; 4)
+ * (`info` holds 16 entries; ABI 1.7, 15 before.)  Same shape/parameter errors as ih_integral_histogram. */
 ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,
                            int32_t kernel, int32_t aligned16, int64_t *info);
 
@@ -131,7 +132,8 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
  * bit 2: skewed segments -- tail_pct is then the percent of segments that
  * are dispatched first and tail_div (> 100) their size ratio x 100 to the
  * rest, so the older CTA of a co-resident pair (favoured by the warp
- * scheduler) does proportionally more rows.  Results are identical for
+ * scheduler) does proportionally more rows; bit 3 / bit 4: bin pairs (two
+ * rows per packed word, each CTA writing 2 bin planes) / bin quads.  Results are identical for
  * every choice; only speed changes.  nseg = 0 removes the hint.  A small
  * process-wide table guarded by a mutex; device.autotune() fills it. */
 ih_status ih_plan_hint(int64_t frames, int64_t height, int64_t width, int32_t slab_bins,

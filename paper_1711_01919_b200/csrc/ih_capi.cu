@@ -87,6 +87,8 @@ constexpr int32_t kHintCluster = 1;  // ih_plan_hint flags: cluster (DSMEM) carr
 constexpr int32_t kHintSmall = 2;    // ih_plan_hint flags: K2s one-launch path
 constexpr int32_t kHintSkew = 4;     // ih_plan_hint flags: skewed segments (tail_pct = % of
                                      // big segments, tail_div = size ratio x 100)
+constexpr int32_t kHintKb2 = 8;      // ih_plan_hint flags: bin pairs (2 rows per packed word)
+constexpr int32_t kHintKb4 = 16;     // ih_plan_hint flags: bin quads (the 4-bin group kernel)
 constexpr int kMaxHints = 64;
 PlanHint g_hints[kMaxHints];
 int g_nhints = 0;
@@ -412,6 +414,19 @@ K2Plan plan_k2_uncached(int64_t frames, int64_t H, int64_t W, int nb, bool vec, 
                             env_int("IH_NO_ROWPACK", 0) == 0 && env_int("IH_CARRY_LOOKBACK", 0) == 0 &&
                             env_int("IH_CARRY_CLUSTER", 0) == 0 && !(fl & kHintCluster);
     p.kb = rowpack_ok && nb <= 2 ? nb : ih::kGroup;
+    // bin pairs with two rows per packed word for >= 24 bins on rows wider
+    // than 512 with aligned stores and >= 256 bin pairs over the frames: each CTA
+    // then writes 2 bin planes instead of 4 for the same scan work per
+    // output, a store pattern HBM drains faster (round-2 A/B, profiles/r02k/:
+    // HD x 64 bench step 0.979 -> 0.983-0.991, its 4-GPU share 0.947 ->
+    // 0.983; 1600x900x64 graph-timed 0.915 -> 0.953; loses for 512-wide
+    // rows, < 24 bins, odd widths and the 8-frame share, 0.944 -> 0.926).
+    // IH_KB=1/2/4 or the plan-hint flags (autotuner) choose explicitly.
+    const int64_t kb_env = env_int("IH_KB", (fl & kHintKb2) ? 2 : (fl & kHintKb4) ? 4 : 0);
+    if (rowpack_ok && kb_env == 0 && nb >= 24 && nchunks > 4 && vec &&
+        frames * ((nb + 1) / 2) >= 256)
+      p.kb = 2;
+    if (rowpack_ok && (kb_env == 1 || kb_env == 2 || kb_env == 4)) p.kb = (int)kb_env;
     if (p.kb < ih::kGroup) p.R = 4;
   }
   p.ngroups = (nb + p.kb - 1) / p.kb;
@@ -1130,7 +1145,7 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   const bool tma = aligned16 != 0 && !knobs().no_tma;
   K2Plan p = plan_k2(frames, height, width, slab_bins, width % 4 == 0, tma);
   const int k = resolve_kernel(kernel, p);
-  for (int i = 0; i < 15; ++i) info[i] = 0;
+  for (int i = 0; i < 16; ++i) info[i] = 0;
   info[0] = k;
   if (k == IH_KERNEL_CROSSWEAVE) {
     info[1] = height > 1 ? 2 : 1;
@@ -1154,6 +1169,7 @@ ih_status ih_plan_describe(int64_t frames, int64_t height, int64_t width, int32_
   info[12] = p.nbig;
   info[13] = p.S2;
   info[14] = p.small ? 4 : p.carry;  // ih::Carry, 4 = K2s in-kernel carries
+  info[15] = p.kb;
   return IH_OK;
 }
 
@@ -1425,7 +1441,7 @@ const char* ih_status_string(ih_status s) {
 
 const char* ih_last_error(void) { return g_last_error; }
 
-int32_t ih_abi_version(void) { return (1 << 16) | 6; }
+int32_t ih_abi_version(void) { return (1 << 16) | 7; }
 
 void* ih_host_alloc(size_t bytes) {
   void* p = nullptr;

@@ -161,7 +161,7 @@ def workspace_bytes(frames: int, height: int, width: int, slab_bins: int, kernel
 PLAN_FIELDS = ("kernel", "launches", "segments", "segment_rows", "chunks_per_lane",
                "rows_per_batch", "warps_per_cta", "workspace_bytes", "column_tiles", "tile_width",
                "resident_ctas", "ctas_per_segment", "big_segments", "tail_segment_rows",
-               "carry")
+               "carry", "bins_per_cta")
 CARRIES = {0: "none", 1: "table", 2: "lookback", 3: "cluster", 4: "in_kernel"}
 
 
@@ -179,14 +179,16 @@ def plan(frames: int, height: int, width: int, slab_bins: int, kernel: str = "au
 
 def set_plan_hint(frames: int, height: int, width: int, slab_bins: int, segments: int,
                   tail_pct: int = 0, tail_div: int = 0, cluster: bool = False,
-                  small: bool = False, skew: bool = False) -> None:
+                  small: bool = False, skew: bool = False, kb: int = 0) -> None:
     """Pin the row-segment count (optional tail split, optional cluster/DSMEM
     carries, or the K2s one-launch kernel with its own segmentation) for one
     problem shape; segments = 0 removes the pin.  ``skew=True`` reads
     (tail_pct, tail_div) as (percent of segments dispatched first, their size
     ratio x 100 to the rest): skewed segments that let the older and the
-    younger CTA of an SM finish together."""
-    flags = (1 if cluster else 0) | (2 if small else 0) | (4 if skew else 0)
+    younger CTA of an SM finish together.  ``kb`` = 2 / 4 pins bin pairs
+    (two rows per packed word) or bin quads where the plan allows either."""
+    flags = (1 if cluster else 0) | (2 if small else 0) | (4 if skew else 0) | \
+        (8 if kb == 2 else 16 if kb == 4 else 0)
     _native.check(_native.lib().ih_plan_hint(frames, height, width, slab_bins, int(segments),
                                              int(tail_pct), int(tail_div), flags))
 
@@ -220,7 +222,8 @@ def load_tuning(path: str) -> int:
     for row in doc["hints"]:
         frames, height, width, nb, segs, tail_pct, tail_div = row[:7]
         flags = row[7] if len(row) > 7 else 0
-        set_plan_hint(frames, height, width, nb, segs, tail_pct, tail_div, skew=bool(flags & 4))
+        set_plan_hint(frames, height, width, nb, segs, tail_pct, tail_div, skew=bool(flags & 4),
+                      kb=2 if flags & 8 else 4 if flags & 16 else 0)
         _TUNED[(frames, height, width, nb)] = (segs, tail_pct, tail_div, flags)
     return len(doc["hints"])
 
@@ -247,9 +250,11 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
              candidates=None, reps: int = 5, images=None, out=None, objective: str = "call") -> dict:
     """Measure integral_histogram (prepare + scan, CUDA-graph replay) for each
     candidate row-segment count on random frames of this shape, then tail
-    splits (10/20/30 % of the rows in quarter-height segments run last) for the
+    splits (10/20/30 % of the rows in quarter-height segments run last), skewed
+    segments and (objective "call") the other bins-per-CTA grouping for the
     best count; pin the fastest with set_plan_hint and return
-    {"segments", "tail_pct", "tail_div", "ms": {"count[/t<pct>]": ms}}.
+    {"segments", "tail_pct", "tail_div", "skew", "bins_per_cta",
+    "ms": {"count[/t<pct>|/s<skew>][/kb<k>]": ms}}.
     Results are bit-identical for every count; only the speed differs.
     ``images`` / ``out`` (CUDA tensors of the call's shapes) avoid allocating
     a second input and output.  ``objective="scan"`` times the scan kernel
@@ -280,8 +285,12 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
     side = torch.cuda.Stream(dev)
     times = {}
 
+    def hint(n, tail_pct=0, tail_div=0, flags=0):
+        set_plan_hint(frames, height, width, nb, n, tail_pct, tail_div, skew=bool(flags & 4),
+                      kb=2 if flags & 8 else 4 if flags & 16 else 0)
+
     def measure(n, tail_pct=0, tail_div=0, flags=0):
-        set_plan_hint(frames, height, width, nb, n, tail_pct, tail_div, skew=bool(flags & 4))
+        hint(n, tail_pct, tail_div, flags)
         need = workspace_bytes(frames, height, width, nb)
         w = ws if ws.numel() >= need else torch.empty(need, dtype=torch.uint8, device=dev)
         for _ in range(2):  # warm: attributes, caches
@@ -319,20 +328,37 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
         if n0 > 1:
             for tail_pct, tail_div, flags in ((10, 4, 0), (20, 4, 0), (30, 4, 0),
                                               (50, 115, 4), (50, 130, 4), (50, 150, 4)):
-                set_plan_hint(frames, height, width, nb, n0, tail_pct, tail_div, skew=bool(flags))
+                hint(n0, tail_pct, tail_div, flags)
                 p = plan(frames, height, width, nb)
                 if p["big_segments"] < p["segments"]:  # the split applies to this shape
                     times[(n0, tail_pct, tail_div, flags)] = measure(n0, tail_pct, tail_div, flags)
+        # third stage (whole calls only): the other bins-per-CTA grouping
+        # (pairs <-> quads) for the best split so far, at every candidate
+        # count (halving the bins per CTA doubles the CTAs).  Not for
+        # objective="scan": a pipeline overlaps consecutive scans, and the
+        # isolated scan time misranks the groupings there (profiles/r02k/:
+        # 8 HD frames x 32 bins, pairs 2 % faster alone, 4 % slower per step)
+        b = min(times, key=times.get)
+        hint(*b)
+        kb0 = plan(frames, height, width, nb)["bins_per_cta"]
+        if kb0 in (2, 4) and objective == "call":
+            other = 16 if kb0 == 2 else 8
+            for n in sorted({b[0]} | set(candidates)):
+                hint(n, b[1], b[2], (b[3] & 4) | other)
+                if plan(frames, height, width, nb)["bins_per_cta"] == 6 - kb0 and \
+                        workspace_bytes(frames, height, width, nb) <= ws.numel():
+                    times[(n, b[1], b[2], (b[3] & 4) | other)] = measure(n, b[1], b[2], (b[3] & 4) | other)
     best = min(times, key=times.get)
-    set_plan_hint(frames, height, width, nb, *best[:3], skew=bool(best[3] & 4))
+    hint(*best)
     _TUNED[(frames, height, width, nb)] = tuple(best)
 
     def key(k):
-        if k[3] & 4:
-            return f"{k[0]}/s{k[2]}"
-        return f"{k[0]}" + (f"/t{k[1]}" if k[1] else "")
+        s = f"{k[0]}/s{k[2]}" if k[3] & 4 else f"{k[0]}" + (f"/t{k[1]}" if k[1] else "")
+        return s + ("/kb2" if k[3] & 8 else "/kb4" if k[3] & 16 else "")
     return {"segments": best[0], "tail_pct": best[1], "tail_div": best[2],
-            "skew": bool(best[3] & 4), "ms": {key(k): round(v, 4) for k, v in times.items()}}
+            "skew": bool(best[3] & 4),
+            "bins_per_cta": 2 if best[3] & 8 else 4 if best[3] & 16 else None,
+            "ms": {key(k): round(v, 4) for k, v in times.items()}}
 
 
 class GraphedIntegralHistogram:

@@ -223,3 +223,34 @@ def test_k2s_plans(monkeypatch):
     assert device.plan(1, 512, 512, 32)["carry"] == "in_kernel"
     monkeypatch.setenv("IH_SMALL", "0")
     assert device.plan(1, 512, 512, 16)["carry"] != "in_kernel"
+
+
+def test_bins_per_cta_plans(monkeypatch):
+    """Bin pairs (two rows per packed word) for >= 24 bins on aligned rows
+    wider than 512 with >= 256 bin pairs over the frames; quads otherwise;
+    1-/2-bin slabs pack rows; IH_KB and the hint flags choose explicitly."""
+    from paper_1711_01919_b200 import device
+
+    kb = lambda *a, **k: device.plan(*a, **k)["bins_per_cta"]  # noqa: E731
+    assert kb(64, 1080, 1920, 32) == 2      # 64 x 16 pairs
+    assert kb(16, 1080, 1920, 32) == 2      # 16 x 16 = 256
+    assert kb(8, 1080, 1920, 32) == 4       # 8 x 16 = 128: quads
+    assert kb(64, 1080, 1920, 16) == 4      # < 24 bins
+    assert kb(64, 512, 512, 32) == 4        # 512-wide rows
+    assert kb(64, 1080, 1918, 32) == 4      # unaligned output rows
+    assert kb(1, 8192, 8192, 256) == 4      # column tiles
+    assert kb(64, 1080, 1920, 1) == 1 and kb(64, 1080, 1920, 2) == 2
+    q, p = device.plan(8, 1080, 1920, 32), device.plan(64, 1080, 1920, 32)
+    monkeypatch.setenv("IH_KB", "2")
+    assert kb(8, 1080, 1920, 32) == 2
+    monkeypatch.setenv("IH_KB", "4")
+    assert kb(64, 1080, 1920, 32) == 4
+    monkeypatch.delenv("IH_KB")
+    device.set_plan_hint(8, 1080, 1920, 32, q["segments"], kb=2)
+    device.set_plan_hint(64, 1080, 1920, 32, p["segments"], kb=4)
+    try:
+        assert kb(8, 1080, 1920, 32) == 2 and kb(64, 1080, 1920, 32) == 4
+    finally:
+        device.set_plan_hint(8, 1080, 1920, 32, 0)
+        device.set_plan_hint(64, 1080, 1920, 32, 0)
+    assert kb(8, 1080, 1920, 32) == 4 and kb(64, 1080, 1920, 32) == 2
