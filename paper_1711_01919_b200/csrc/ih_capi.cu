@@ -802,24 +802,45 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
                        ? (uint32_t*)((uint8_t*)ws + k2_table_bytes(c.frames, p) +
                                      k2_rowleft_bytes(c.frames, c.H, p))
                        : nullptr;
+  // column chunks per count CTA (one per warp, the other warps split the rows):
+  // the largest power of two <= 8 chunks of the row whose per-chunk shared
+  // tables stay <= 40 KB and whose grid still has >= 8 CTAs per SM (HD x 64 x
+  // 1 bin, 20 segments: 8 chunks per CTA, 81 -> 61 us; one 4K frame of 16 bins
+  // over 37 segments needs 1: 4 CTAs over 36 x 30 chunks under-fill the SMs).
+  // IH_COUNT_CW forces 1/2/4/8.
+  const int64_t nch = p.Wp / ih::kChunk;
+  // (rows of loads in flight per warp: 8; 16 measured no faster, profiles/r02l/)
+  auto count_cw = [&](size_t table_bytes) {
+    const int64_t rows_of_ctas = (int64_t)(p.nseg - 1) * c.frames;
+    int cw = 8;
+    while (cw > 1 && (cw > nch || (size_t)cw * table_bytes > (40u << 10) ||
+                      (nch + cw - 1) / cw * rows_of_ctas < 8 * (int64_t)device_sms()))
+      cw >>= 1;
+    const int64_t force = env_int("IH_COUNT_CW", 0);
+    if (force == 1 || force == 2 || force == 4 || force == 8) cw = (int)force;
+    return cw;
+  };
   if (p.nbp <= ih::kGroup && !p.colt && env_int("IH_COLCOUNTS_G1", 1) != 0 &&
       !knobs().colcounts_slab) {  // one group of <= 4 bins: counts in registers
-    dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
-    auto kern = al ? ih::k2_colcounts_g1<true> : ih::k2_colcounts_g1<false>;
+    const int cw = count_cw(0);
+    dim3 grid((unsigned)((nch + cw - 1) / cw), (unsigned)(p.nseg - 1), (unsigned)c.frames);
+    auto kern = al ? ih::k2_colcounts_g1<true, 8> : ih::k2_colcounts_g1<false, 8>;
     if (launch(kern, grid, dim3(256), 0, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch, c.fstride,
-               c.lut, segs(p), p.nseg, p.nbp, p.Wp, (uint16_t*)ws) != cudaSuccess)
+               c.lut, segs(p), p.nseg, p.nbp, p.Wp, cw, (uint16_t*)ws) != cudaSuccess)
       return cuda_fail("k2_colcounts_g1");
     ++c.launched;
     return launch_colprefix(c, ws);
   }
   if (!knobs().colcounts_slab) {  // all bins in one pass (shared atomics)
-    dim3 grid((unsigned)(p.Wp / ih::kChunk), (unsigned)(p.nseg - 1), (unsigned)c.frames);
-    auto kern = al ? ih::k2_colcounts_all<true> : ih::k2_colcounts_all<false>;
-    const size_t smem = (size_t)(p.nbp + 1) * 64 * sizeof(uint32_t);
+    const size_t table = (size_t)(p.nbp + 1) * 64 * sizeof(uint32_t);
+    const int cw = count_cw(table);
+    dim3 grid((unsigned)((nch + cw - 1) / cw), (unsigned)(p.nseg - 1), (unsigned)c.frames);
+    auto kern = al ? ih::k2_colcounts_all<true, 8> : ih::k2_colcounts_all<false, 8>;
+    const size_t smem = cw * table;
     if (!set_dyn_smem((const void*)kern, smem))
       return cuda_fail("k2_colcounts_all smem attribute");
     if (launch(kern, grid, dim3(256), smem, c.stream, c.pdl(), c.img, c.H, c.W, c.pitch,
-               c.fstride, c.lut, segs(p), p.nseg, p.nbp, p.Wp, (uint16_t*)ws, ctot) != cudaSuccess)
+               c.fstride, c.lut, segs(p), p.nseg, p.nbp, p.Wp, cw, (uint16_t*)ws, ctot) != cudaSuccess)
       return cuda_fail("k2_colcounts_all");
     ++c.launched;
     return launch_colprefix(c, ws);

@@ -31,7 +31,7 @@ struct Segs {
 
 // Per-call binning table: relative bin (lut[v] - bin_lo) or 0xFF when the
 // bin lies outside the slab [bin_lo, bin_hi).  Passed by value (kernel param).
-struct RelLut {
+struct alignas(16) RelLut {  // 16-byte aligned: kernels copy it out as words
   uint8_t rel[256];
 };
 

@@ -159,19 +159,48 @@ __device__ __forceinline__ void red_shared_add(uint32_t saddr, uint32_t v) {
   asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(saddr), "r"(v) : "memory");
 }
 
-template <bool ALIGNED>
+// The last n < U rows of a count loop (rows p, p + rstep, ...): loads for
+// binary sub-batches of n (U/2, ..., 2, 1 rows, warp-uniform branches) are
+// all issued before any row is counted -- one load latency, and unlike one
+// predicated U-row batch, no predicated-off counting work for short tails.
+template <int U, typename Load, typename Use>
+__device__ __forceinline__ void tail_rows(int n, const uint8_t* p, int64_t rstep, Load load,
+                                          Use use) {
+  uint32_t px[U];
+  int at = 0;
+#pragma unroll
+  for (int b = U / 2; b >= 1; b >>= 1)
+    if (n & b) {
+#pragma unroll
+      for (int i = 0; i < b; ++i) px[(U - 2 * b) + i] = load(p + (int64_t)(at + i) * rstep);
+      at += b;
+    }
+#pragma unroll
+  for (int b = U / 2; b >= 1; b >>= 1)
+    if (n & b) {
+#pragma unroll
+      for (int i = 0; i < b; ++i) use(px[(U - 2 * b) + i]);
+    }
+}
+
+template <bool ALIGNED, int U>
 __global__ void __launch_bounds__(256) k2_colcounts_all(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
-    RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws,
+    RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, int cw, uint16_t* __restrict__ ws,
     uint32_t* __restrict__ ctot) {
-  extern __shared__ __align__(16) uint32_t hist2[];  // [nbp + 1][2][32]: row nbp = discard
+  // [cw][nbp + 1][2][32]: one table per column chunk of the CTA, row nbp = discard
+  extern __shared__ __align__(16) uint32_t hist2[];
   __shared__ uint32_t sw[512];  // pixel (| 256 past the edge) -> word offset of its bin row
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int nw = blockDim.x >> 5;
-  const int64_t c = (int64_t)blockIdx.x * kChunk + 4 * lane;
+  // warp -> (column chunk wc of the CTA's cw, row phase of 8 / cw): whole
+  // chunks per warp keep 8 rows of loads in flight even on short segments
+  const int lg = __ffs(cw) - 1, wc = warp & (cw - 1), rs = 8 >> lg, phase = warp >> lg;  // cw = 2^lg
+  const int64_t nch = Wp / kChunk;
+  const int64_t c = ((int64_t)blockIdx.x * cw + wc) * kChunk + 4 * lane;
   const int s = blockIdx.y;
   const int64_t f = blockIdx.z;
+  const int tw = (nbp + 1) * 64;  // words per chunk table
   griddep_launch_dependents();
   for (int v = threadIdx.x; v < 512; v += blockDim.x) {
     const uint32_t b = v < 256 ? (uint32_t)lut.rel[v] : 0xffffffffu;
@@ -179,14 +208,13 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
   }
   {
     uint4* z = reinterpret_cast<uint4*>(hist2);
-    for (int i = threadIdx.x; i < (nbp + 1) * 16; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
+    for (int i = threadIdx.x; i < cw * tw / 4; i += blockDim.x) z[i] = make_uint4(0, 0, 0, 0);
   }
   uint32_t inval[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) inval[k] = (c + k < W) ? 0u : 256u;
   __syncthreads();
-  uint32_t* hl = hist2 + lane;
-  const uint32_t hs = (uint32_t)__cvta_generic_to_shared(hl);
+  const uint32_t hs = (uint32_t)__cvta_generic_to_shared(hist2 + wc * tw + lane);
   const uint8_t* base = img + f * fstride;
   const int64_t seg0 = sg.start(s);
   const int64_t seg1 = min(sg.start(s + 1), H);
@@ -206,14 +234,13 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
     }
   };
   if (c < W) {
-    // rows seg0 + warp + i*nw; 8 rows of loads in flight per warp, addressed
+    // rows seg0 + phase + i*rs; 8 rows of loads in flight per warp, addressed
     // by stepping one row pointer (no 64-bit multiply per load); a 32-bit row
-    // count (segments are < 65536 rows) and predicates only on the last < 8
-    constexpr int U = 8;
-    const int64_t rstep = (int64_t)nw * pitch;
+    // count (segments are < 65536 rows)
+    const int64_t rstep = (int64_t)rs * pitch;
     const int nrows = (int)(seg1 - seg0);
-    const int mine = nrows > warp ? (nrows - warp + nw - 1) / nw : 0;
-    const uint8_t* p = base + (seg0 + warp) * pitch + c;
+    const int mine = nrows > phase ? (nrows - phase + rs - 1) / rs : 0;
+    const uint8_t* p = base + (seg0 + phase) * pitch + c;
     for (int it = 0; it < mine / U; ++it, p += U * rstep) {
       uint32_t px[U];
 #pragma unroll
@@ -221,19 +248,25 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
 #pragma unroll
       for (int i = 0; i < U; ++i) count4(px[i]);
     }
-    for (int i = 0; i < mine % U; ++i, p += rstep) count4(load_px(p));
+    // the last < U rows: all loads in flight at once (a row-at-a-time loop
+    // serialises on the load latency), without predicated-off work
+    tail_rows<U>(mine % U, p, rstep, load_px, count4);
   }
   __syncthreads();
   griddep_wait();  // PDL: complete only after the predecessor (transitivity)
-  uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp) * Wp + (int64_t)blockIdx.x * kChunk;
-  uint32_t* tdst = ctot ? ctot + ((f * nseg + s) * (int64_t)gridDim.x + blockIdx.x) * nbp : nullptr;
-  for (int e = threadIdx.x; e < nbp * 32; e += blockDim.x) {  // warp-uniform bin b
-    const int l = e & 31, b = e >> 5;
-    const uint32_t w0 = hist2[(b * 2) * 32 + l], w1 = hist2[(b * 2 + 1) * 32 + l];
-    *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) = make_uint2(w0, w1);
-    if (tdst) {  // column-tiled scans: the chunk's total per bin
-      const uint32_t sum = __reduce_add_sync(kFull, (w0 & 0xffffu) + (w0 >> 16) + (w1 & 0xffffu) + (w1 >> 16));
-      if (l == 0) tdst[b] = sum;
+  for (int k = 0; k < cw; ++k) {
+    const int64_t ch = (int64_t)blockIdx.x * cw + k;
+    if (ch >= nch) break;
+    const uint32_t* h = hist2 + k * tw;
+    uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp) * Wp + ch * kChunk;
+    for (int e = threadIdx.x; e < nbp * 32; e += blockDim.x) {  // warp-uniform bin b
+      const int l = e & 31, b = e >> 5;
+      const uint32_t w0 = h[(b * 2) * 32 + l], w1 = h[(b * 2 + 1) * 32 + l];
+      *reinterpret_cast<uint2*>(dst + (int64_t)b * Wp + 4 * l) = make_uint2(w0, w1);
+      if (ctot) {  // column-tiled scans: the chunk's total per bin
+        const uint32_t sum = __reduce_add_sync(kFull, (w0 & 0xffffu) + (w0 >> 16) + (w1 & 0xffffu) + (w1 >> 16));
+        if (l == 0) ctot[((f * nseg + s) * nch + ch) * nbp + b] = sum;
+      }
     }
   }
 }
@@ -243,19 +276,24 @@ __global__ void __launch_bounds__(256) k2_colcounts_all(
 // e.g. B = 1 / 2 / 4): counting in registers instead of shared atomics.  A
 // lane's 4 columns take one one-hot word per pixel (the scan's packed-byte
 // table: one byte per bin of the group), added byte-wise into 4 registers and
-// widened into 16-bit lanes every 255 rows; the 8 warps' column counts are
-// summed through shared memory and dumped as the u16 table rows of the slab's
-// <= 4 bins.  Same grid and output as k2_colcounts_all (no column tiles).
+// widened into 16-bit lanes every 248 rows.  Warps map to (column chunk, row
+// phase) as in k2_colcounts_all; the row phases of a chunk are summed through
+// shared memory and dumped as the u16 table rows of the slab's <= 4 bins.
+// (Slower, profiles/r02l/: a warp-shuffle bin lookup, 81 -> 91 us on HD x 64
+// x 1 bin; a conflict-free lane-replicated 32 KB table, 61 -> 77 us.)  Same output as k2_colcounts_all (no
+// column tiles).
 // ---------------------------------------------------------------------------
-template <bool ALIGNED>
+template <bool ALIGNED, int U>
 __global__ void __launch_bounds__(256) k2_colcounts_g1(
     const uint8_t* __restrict__ img, int64_t H, int64_t W, int64_t pitch, int64_t fstride,
-    RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, uint16_t* __restrict__ ws) {
+    RelLut lut, Segs sg, int nseg, int nbp, int64_t Wp, int cw, uint16_t* __restrict__ ws) {
   __shared__ uint32_t oh[kOneHotEntries];
   __shared__ uint4 part[8][2][32];  // [warp][bins 0/2 | 1/3][lane] 16-bit lanes, 4 columns
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
-  const int64_t c = (int64_t)blockIdx.x * kChunk + 4 * lane;
+  const int lg = __ffs(cw) - 1, wc = warp & (cw - 1), rs = 8 >> lg, phase = warp >> lg;  // cw = 2^lg
+  const int64_t nch = Wp / kChunk;
+  const int64_t c = ((int64_t)blockIdx.x * cw + wc) * kChunk + 4 * lane;
   const int s = blockIdx.y;
   const int64_t f = blockIdx.z;
   griddep_launch_dependents();
@@ -268,12 +306,12 @@ __global__ void __launch_bounds__(256) k2_colcounts_g1(
   const int64_t seg1 = min(sg.start(s + 1), H);
   uint32_t ce[4] = {0u, 0u, 0u, 0u}, co[4] = {0u, 0u, 0u, 0u};
   if (c < W) {
-    // this warp's rows: seg0 + warp + 8 i (32-bit counters: segments are
-    // < 65536 rows), pointer-stepped, predicates only on the last < 8 rows
+    // this warp's rows: seg0 + phase + rs i (32-bit counters: segments are
+    // < 65536 rows), pointer-stepped
     const int nrows = (int)(seg1 - seg0);
-    int left = nrows > warp ? (nrows - warp + 7) / 8 : 0;
-    const uint8_t* q = img + f * fstride + (seg0 + warp) * pitch + c;
-    const int64_t rstep = 8 * pitch;
+    int left = nrows > phase ? (nrows - phase + rs - 1) / rs : 0;
+    const uint8_t* q = img + f * fstride + (seg0 + phase) * pitch + c;
+    const int64_t rstep = rs * pitch;
     auto load_px = [&](const uint8_t* row) -> uint32_t {
       if (ALIGNED) return __ldg(reinterpret_cast<const uint32_t*>(row));
       uint32_t px = 0;
@@ -286,7 +324,6 @@ __global__ void __launch_bounds__(256) k2_colcounts_g1(
 #pragma unroll
       for (int k = 0; k < 4; ++k) acc[k] += oh[((px >> (8 * k)) & 0xffu) | inval[k]];
     };
-    constexpr int U = 8;
     while (left > 0) {
       // byte-packed counts: <= 248 rows (31 x 8) per flush into 16-bit lanes
       const int chunk = left < 248 ? left : 248;
@@ -299,7 +336,9 @@ __global__ void __launch_bounds__(256) k2_colcounts_g1(
         for (int i = 0; i < U; ++i) add4(px[i], acc);
         q += U * rstep;
       }
-      for (int i = 0; i < chunk % U; ++i, q += rstep) add4(load_px(q), acc);
+      const int rem = chunk % U;  // all loads in flight at once (tail_rows)
+      tail_rows<U>(rem, q, rstep, load_px, [&](uint32_t px) { add4(px, acc); });
+      q += rem * rstep;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         ce[k] += acc[k] & 0x00ff00ffu;
@@ -312,20 +351,22 @@ __global__ void __launch_bounds__(256) k2_colcounts_g1(
   part[warp][1][lane] = make_uint4(co[0], co[1], co[2], co[3]);
   __syncthreads();
   griddep_wait();  // PDL: complete only after the predecessor (transitivity)
-  if (warp < 2) {  // warp 0: bins 0/2, warp 1: bins 1/3
+  for (int e = threadIdx.x; e < cw * 64; e += blockDim.x) {  // (chunk k, half h: bins h / h + 2)
+    const int l = e & 31, h = (e >> 5) & 1, k = e >> 6;
+    const int64_t ch = (int64_t)blockIdx.x * cw + k;
+    if (ch >= nch) break;
     uint4 t = make_uint4(0u, 0u, 0u, 0u);
-#pragma unroll
-    for (int w = 0; w < 8; ++w) {
-      const uint4 x = part[w][warp][lane];
+    for (int r = 0; r < rs; ++r) {
+      const uint4 x = part[r * cw + k][h][l];
       t.x += x.x; t.y += x.y; t.z += x.z; t.w += x.w;
     }
-    uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp) * Wp + (int64_t)blockIdx.x * kChunk + 4 * lane;
-    // 16-bit lanes: low half = bin `warp`, high half = bin `warp + 2`
-    if (warp < nbp)
-      *reinterpret_cast<uint2*>(dst + (int64_t)warp * Wp) =
+    uint16_t* dst = ws + ((f * nseg + s) * (int64_t)nbp) * Wp + ch * kChunk + 4 * l;
+    // 16-bit lanes: low half = bin h, high half = bin h + 2
+    if (h < nbp)
+      *reinterpret_cast<uint2*>(dst + (int64_t)h * Wp) =
           make_uint2(__byte_perm(t.x, t.y, 0x5410), __byte_perm(t.z, t.w, 0x5410));
-    if (warp + 2 < nbp)
-      *reinterpret_cast<uint2*>(dst + (int64_t)(warp + 2) * Wp) =
+    if (h + 2 < nbp)
+      *reinterpret_cast<uint2*>(dst + (int64_t)(h + 2) * Wp) =
           make_uint2(__byte_perm(t.x, t.y, 0x7632), __byte_perm(t.z, t.w, 0x7632));
   }
 }

@@ -17,12 +17,14 @@ envs = [{}, {"IH_NSEG": "3"}, {"IH_NSEG": "5", "IH_TABLE_SUM_MAX": "1"},
         {"IH_NSEG": "3", "IH_NO_COLTILE": "1"}, {"IH_NSEG": "4", "IH_TAIL_PCT": "30"},
         {"IH_NSEG": "3", "IH_CARRY_CLUSTER": "1"}, {"IH_NSEG": "2", "IH_STAGED_STORES": "1"},
         {"IH_SMALL": "1"}, {"IH_SMALL": "1", "IH_NSEG": "7"},
-        {"IH_NSEG": "5", "IH_SKEW_X100": "130"}, {"IH_NSEG": "4", "IH_COLCOUNTS_G1": "0"}]
+        {"IH_NSEG": "5", "IH_SKEW_X100": "130"}, {"IH_NSEG": "4", "IH_COLCOUNTS_G1": "0"},
+        {"IH_NSEG": "9", "IH_COUNT_CW": "2"}, {"IH_NSEG": "7", "IH_KB": "2"}]
 bad = 0
 for env in envs:
     for k in ("IH_NSEG", "IH_TABLE_SUM_MAX", "IH_CARRY_LOOKBACK", "IH_NO_TMA", "IH_ROWS_PER_BATCH",
               "IH_COLCOUNTS_SLAB", "IH_NO_COLTILE", "IH_TAIL_PCT", "IH_CARRY_CLUSTER",
-              "IH_STAGED_STORES", "IH_SMALL", "IH_SKEW_X100", "IH_COLCOUNTS_G1"):
+              "IH_STAGED_STORES", "IH_SMALL", "IH_SKEW_X100", "IH_COLCOUNTS_G1", "IH_COUNT_CW",
+              "IH_KB"):
         os.environ.pop(k, None)
     os.environ.update(env)
     for (h, w, b) in cases:

@@ -19,7 +19,7 @@ KNOBS = ("IH_NSEG", "IH_TAIL_PCT", "IH_TAIL_DIV", "IH_CARRY_LOOKBACK", "IH_CARRY
          "IH_TABLE_SUM_MAX", "IH_ROWS_PER_BATCH", "IH_NO_TMA", "IH_NO_COLTILE", "IH_TILE_CHUNKS",
          "IH_COLCOUNTS_SLAB", "IH_NO_PDL", "IH_MIN_SEG_ROWS", "IH_K4_MODE", "IH_K5_DIRECT",
          "IH_STAGED_STORES", "IH_NO_RESTAGE", "IH_NO_ROWPACK", "IH_SMALL", "IH_SKEW_X100",
-         "IH_SKEW_PCT", "IH_COLCOUNTS_G1", "IH_K5_CHAIN")
+         "IH_SKEW_PCT", "IH_COLCOUNTS_G1", "IH_K5_CHAIN", "IH_COUNT_CW", "IH_KB")
 
 
 def _case(rng):
@@ -60,6 +60,10 @@ def _case(rng):
     offset = int(rng.choice([0, 0, 1, 3]))
     if rng.random() < 0.5:  # unaligned rows: the kernels' own LDG path
         env["IH_NO_RESTAGE"] = "1"
+    if rng.random() < 0.3:  # column chunks per count CTA (warps per chunk 8 / cw)
+        env["IH_COUNT_CW"] = str(int(rng.choice([1, 2, 4, 8])))
+    if rng.random() < 0.2:  # bins per scan CTA where row packing applies
+        env["IH_KB"] = str(int(rng.choice([1, 2, 4])))
     return H, W, bins, lo, hi, env, offset
 
 
