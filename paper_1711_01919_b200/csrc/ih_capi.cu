@@ -1092,14 +1092,31 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   const int64_t R = height - h + 1, C = width - w + 1;
   const int threads = C >= 1024 ? 256 : (int)((C + 127) / 128 * 32);
   const size_t smem = (size_t)(4 * threads + w) * sizeof(uint32_t);
-  // IH_K4_MODE 3 (default): pairs of adjacent outputs per 16-byte store;
+  // IH_K4_MODE 3: pairs of adjacent outputs per 16-byte store;
   // 1: 4 strided outputs per thread; 0: the two-output kernel; 2: staged row
   // differences (while CW + w u32 fit in shared memory)
   // mode 3's 16-byte pair stores need a 16-byte aligned `out`; int64 views
   // at odd element offsets take the 8-byte-store kernel (mode 1)
-  int64_t k4mode = env_int("IH_K4_MODE", 3);
+  // mode 4 (default where it applies): 4 adjacent outputs per thread from
+  // 16-byte corner loads -- needs 16-byte aligned tensor rows (W % 4 == 0)
+  // and a 16-byte aligned `out`; otherwise mode 3
+  int64_t k4mode = env_int("IH_K4_MODE", 4);
+  if (k4mode == 4 && (width % 4 != 0 || ((uintptr_t)t & 15) || ((uintptr_t)out & 15))) k4mode = 3;
   if (k4mode == 3 && ((uintptr_t)out & 15)) k4mode = 1;
   if ((uintptr_t)out & 7) return fail(IH_ERR_PARAM, "out must be 8-byte aligned");
+  if (k4mode == 4) {
+    const int64_t cb = (C + 4 * 256 - 1) / (4 * 256);
+    int64_t ry = (int64_t)device_sms() * env_int("IH_K4_CTAS_PER_SM", 256) / (cb * nb);
+    ry = ry < 1 ? 1 : ry > R ? R : ry > 65535 ? 65535 : ry;
+    dim3 grid((unsigned)cb, (unsigned)ry, (unsigned)nb);
+    const int m = (w - 1) & 3;
+    auto k = m == 0 ? ih::k4_window_counts_quads<0> : m == 1 ? ih::k4_window_counts_quads<1>
+           : m == 2 ? ih::k4_window_counts_quads<2> : ih::k4_window_counts_quads<3>;
+    k<<<grid, 256, 0, (cudaStream_t)stream>>>(t, nb, height, width, h, w,
+                                             reinterpret_cast<long long*>(out));
+    if (cudaPeekAtLastError() != cudaSuccess) return cuda_fail("k4_window_counts_quads");
+    return IH_OK;
+  }
   if (k4mode == 3) {  // two adjacent outputs per 16-byte store
     const int U = env_int("IH_K4_PAIRS_U", 2) == 4 ? 4 : env_int("IH_K4_PAIRS_U", 2) == 1 ? 1 : 2;
     const int64_t cb = (C + 1 + 2 * 256 * U - 1) / (2 * 256 * U);  // U pairs per thread

@@ -177,6 +177,108 @@ __global__ void __launch_bounds__(256, 6) k4_window_counts_pairs(const uint32_t*
   }
 }
 
+// K4 (quads, the default for 16-byte aligned tensor rows): a thread forms 4
+// adjacent outputs j = q..q+3 (q % 4 == 0) of one row.  Their left corners
+// are columns q-1..q+2 (a 16-byte load at q plus one word at q-1) and their
+// right corners columns q+w-1..q+w+2, taken from one or two aligned 16-byte
+// loads at the word offset M = (w - 1) % 4 (a template parameter: no per-row
+// select).  8 loads per 4 outputs instead of 16 scalar corner loads -- the
+// pairs kernel executed 59 instructions per output and was issue bound
+// (profiles/r02c/k4_pairs_summary.json).  Stores: two 16-byte pairs, or a
+// word + pair + word when the output row starts at an odd element.  Threads
+// whose loads would pass the row end take the scalar corner path.
+__device__ __forceinline__ uint4 ldg4(const uint32_t* p) {
+  return __ldg(reinterpret_cast<const uint4*>(p));
+}
+template <int M>
+__device__ __forceinline__ void pick4(const uint4& a, const uint4& b, uint32_t r[4]) {
+  const uint32_t v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) r[k] = v[M + k];
+}
+
+// One row's 4 outputs (see k4_window_counts_quads): corner loads issued by
+// load(), differences and stores by finish(), so a thread can keep several
+// rows' loads in flight.
+template <int M>
+struct K4Quad {
+  uint4 lb, rb0, rb1, lt, rt0, rt1;
+  uint32_t lbm, ltm;
+  __device__ __forceinline__ void load(const uint32_t* bot, const uint32_t* top, int64_t q,
+                                       int64_t a0) {
+    lb = ldg4(bot + q);
+    lbm = q > 0 ? __ldg(bot + q - 1) : 0u;
+    rb0 = ldg4(bot + a0);
+    rb1 = M ? ldg4(bot + a0 + 4) : make_uint4(0u, 0u, 0u, 0u);
+    if (top) {
+      lt = ldg4(top + q);
+      ltm = q > 0 ? __ldg(top + q - 1) : 0u;
+      rt0 = ldg4(top + a0);
+      rt1 = M ? ldg4(top + a0 + 4) : make_uint4(0u, 0u, 0u, 0u);
+    } else {
+      lt = rt0 = rt1 = make_uint4(0u, 0u, 0u, 0u);
+      ltm = 0u;
+    }
+  }
+  __device__ __forceinline__ void finish(long long* o) const {
+    uint32_t rb[4], rt[4], n[4];
+    pick4<M>(rb0, rb1, rb);
+    pick4<M>(rt0, rt1, rt);
+    // exact in u32: each difference is a window count
+    n[0] = (rb[0] - lbm) - (rt[0] - ltm);
+    n[1] = (rb[1] - lb.x) - (rt[1] - lt.x);
+    n[2] = (rb[2] - lb.y) - (rt[2] - lt.y);
+    n[3] = (rb[3] - lb.z) - (rt[3] - lt.z);
+    if ((((uintptr_t)o) & 15) == 0) {
+      __stcs(reinterpret_cast<longlong2*>(o), make_longlong2(n[0], n[1]));
+      __stcs(reinterpret_cast<longlong2*>(o + 2), make_longlong2(n[2], n[3]));
+    } else {
+      __stcs(o, (long long)n[0]);
+      __stcs(reinterpret_cast<longlong2*>(o + 1), make_longlong2(n[1], n[2]));
+      __stcs(o + 3, (long long)n[3]);
+    }
+  }
+};
+
+template <int M>
+__global__ void __launch_bounds__(256) k4_window_counts_quads(const uint32_t* __restrict__ t,
+                                                                int nb, int64_t H, int64_t W,
+                                                                int h, int w,
+                                                                long long* __restrict__ out) {
+  const int64_t R = H - h + 1, C = W - w + 1;
+  const int64_t b = blockIdx.z;
+  const uint32_t* p = t + b * H * W;
+  const int64_t q = 4 * ((int64_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (q >= C) return;
+  const int64_t a0 = q + w - 1 - M;  // 16-byte aligned base of the right corners
+  const bool fast = q + 4 <= C && a0 + (M ? 8 : 4) <= W;
+  const int64_t ry = gridDim.y;
+  if (fast) {
+    // one row per step (two rows i, i + ry per step keep more loads in flight
+    // but were 0.146 -> 0.201 ms: 64 registers, half the CTAs, and twice the
+    // tensor rows live in L2 at a time; profiles/r02l/k4_sweep.jsonl)
+    for (int64_t i = blockIdx.y; i < R; i += ry) {
+      K4Quad<M> x;
+      x.load(p + (i + h - 1) * W, i > 0 ? p + (i - 1) * W : nullptr, q, a0);
+      x.finish(out + (b * R + i) * C + q);
+    }
+    return;
+  }
+  for (int64_t i = blockIdx.y; i < R; i += ry) {
+    const uint32_t* bot = p + (i + h - 1) * W;
+    const uint32_t* top = p + (i - 1) * W;  // used only when i > 0
+    long long* orow = out + (b * R + i) * C;
+    for (int k = 0; k < 4 && q + k < C; ++k) {
+      const int64_t j = q + k;
+      const uint32_t a11 = __ldg(bot + j + w - 1);
+      const uint32_t a10 = j > 0 ? __ldg(bot + j - 1) : 0u;
+      const uint32_t a01 = i > 0 ? __ldg(top + j + w - 1) : 0u;
+      const uint32_t a00 = i > 0 && j > 0 ? __ldg(top + j - 1) : 0u;
+      __stcs(orow + j, (long long)(a11 - a10 - a01 + a00));
+    }
+  }
+}
+
 // Row-difference staging for K4 (the "vs" variant).  For output
 // row i the window count at column j is
 //     V[j + w - 1] - V[j - 1],   V(c) = T(i + h - 1, c) - T(i - 1, c)

@@ -137,7 +137,7 @@ def test_fuzz_queries(monkeypatch, seed):
                               O.region_histograms(full, regs))
         h, w = int(rng.integers(1, H + 1)), int(rng.integers(1, W + 1))
         want = O.window_counts(full, h, w)
-        for mode in ("0", "1", "2", "3"):
+        for mode in ("0", "1", "2", "3", "4"):
             monkeypatch.setenv("IH_K4_MODE", mode)
             assert np.array_equal(device.window_counts(t, h, w).cpu().numpy(), want), (H, W, h, w, mode)
         tmpl = rng.random(bins)

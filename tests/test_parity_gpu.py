@@ -575,15 +575,17 @@ def test_out_argument_and_int32_view(rng):
 
 def test_window_count_kernel_variants(monkeypatch, rng):
     """K4 variants (two-output corners, 4-output ILP corners, staged row
-    differences) against the oracle: bit-identical, including odd output
-    widths, w = W, h = H and 1-pixel windows."""
-    for (H, W, B) in [(70, 1500, 5), (33, 2100, 32), (9, 7, 3), (300, 257, 16)]:
+    differences, 4 outputs from 16-byte corner loads) against the oracle:
+    bit-identical, including odd output widths, w = W, h = H, 1-pixel
+    windows and every right-corner word offset (w - 1) % 4."""
+    for (H, W, B) in [(70, 1500, 5), (33, 2100, 32), (9, 7, 3), (300, 257, 16), (21, 4, 2), (5, 12, 7)]:
         px = rng.integers(0, 256, (H, W), dtype=np.uint8)
         full = O.compute_crossweave(px, O.np_uniform_table(B), B)
         t = torch.from_numpy(full.view(np.int32)).cuda().view(torch.uint32)
-        for (h, w) in [(1, 1), (min(5, H), min(8, W)), (H, W), (H // 2 + 1, W // 3 + 1), (1, W), (H, 1)]:
+        for (h, w) in [(1, 1), (min(5, H), min(8, W)), (H, W), (H // 2 + 1, W // 3 + 1), (1, W), (H, 1),
+                       (min(4, H), min(2, W)), (2, min(3, W)), (H - 1 or 1, max(W - 1, 1))]:
             want = O.window_counts(full, h, w)
-            for mode in ("0", "1", "2", "3"):
+            for mode in ("0", "1", "2", "3", "4"):
                 monkeypatch.setenv("IH_K4_MODE", mode)
                 assert np.array_equal(device.window_counts(t, h, w).cpu().numpy(), want), (H, W, h, w, mode)
 
