@@ -415,16 +415,10 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     stream = torch.cuda.current_stream(dev)
     brange = (b0, b1) if active else None
     tuned = None
-    if args.autotune and active:  # measured row-segment count for this shape (warm-up phase)
-        # the whole call (prepare + scan): tuning the scan alone picked many
-        # short segments whose prepass, even overlapped, cost more (HD x8:
-        # step 0.80 vs 0.88; profiles/r01f/autotune_objective.txt)
-        objective = "call"
-        tuned = device.autotune(nloc, wl.height, wl.width, wl.bins, bin_range=brange, device=dev,
-                                images=d_img[:nloc], out=out[:nloc], objective=objective)
-        tuned["objective"] = objective
-    plan = device.plan(nloc, wl.height, wl.width, nb,
-                       aligned16=d_img.data_ptr() % 16 == 0) if active else {"launches": 0}
+
+    def set_hint(c):  # an autotune candidate [segments, tail_pct, tail_div, flags, ms]
+        device.set_plan_hint(nloc, wl.height, wl.width, nb, c[0], c[1], c[2], skew=bool(c[3] & 4),
+                             kb=2 if c[3] & 8 else 4 if c[3] & 16 else 0)
 
     # Steps are pipelined the way a video stream runs: the prepass of batch k+1
     # (k2_colcounts: reads only the images) runs on a side stream into the
@@ -445,6 +439,19 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
     # flight): with two scan streams, batch k+1's carries are ready when batch
     # k's first CTAs retire, so its scan can start in their slots
     ahead = 2 if len(outs) > 1 else 1
+    if args.autotune and active:  # measured row-segment count for this shape (warm-up phase)
+        # the whole call (prepare + scan): tuning the scan alone picked many
+        # short segments whose prepass, even overlapped, cost more (HD x8:
+        # step 0.80 vs 0.88; profiles/r01f/autotune_objective.txt)
+        objective = "call"
+        tuned = device.autotune(nloc, wl.height, wl.width, wl.bins, bin_range=brange, device=dev,
+                                images=d_img[:nloc], out=out[:nloc], objective=objective)
+        tuned["objective"] = objective
+        # workspaces for every candidate the pipelined refinement below may pick
+        for c in tuned["ranked"][:args.refine]:
+            set_hint(c)
+            nws = max(nws, device.workspace_bytes(nloc, wl.height, wl.width, nb))
+        set_hint(tuned["ranked"][0])
     wss = [torch.empty(nws, dtype=torch.uint8, device=dev) for _ in range(ahead + 1)]
 
     def run_steps(n, ev_scan0=None, ev_scan1=None):
@@ -505,6 +512,27 @@ def run_ours(args, wl: Workload, rank, world, local_rank):
             tot += e0.elapsed_time(e1)
         return tot / n
 
+    if tuned is not None and len(outs) > 1 and args.refine > 1:
+        # pipelined refinement: the call-timed ranking misorders plans whose
+        # scans overlap differently in these steps (8 HD frames: bin pairs 2 %
+        # faster per call, 4 % slower per pipelined step; profiles/r02m/), so
+        # the top candidates run a few real steps each and the fastest is kept
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps_ms = []
+        for c in tuned["ranked"][:args.refine]:
+            set_hint(c)
+            run_steps(2)
+            e0.record(stream)
+            run_steps(6)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            steps_ms.append((e0.elapsed_time(e1) / 6, c))
+        best = min(steps_ms, key=lambda x: x[0])[1]
+        set_hint(best)
+        tuned["pipelined_refine_ms"] = [[round(ms, 4)] + c[:4] for ms, c in steps_ms]
+        tuned["chosen"] = best[:4]
+    plan = device.plan(nloc, wl.height, wl.width, nb,
+                       aligned16=d_img.data_ptr() % 16 == 0) if active else {"launches": 0}
     run_steps(args.warmup)
     barrier()
     with ClockSampler(dev_index) as clocks:
@@ -903,6 +931,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--chunk", type=int, default=4, help="frames per pipelined e2e chunk")
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--refine", type=int, default=4,
+                    help="autotune candidates re-timed as pipelined steps (1: call ranking only)")
     ap.add_argument("--no-autotune", dest="autotune", action="store_false",
                     help="keep the planner's heuristic row-segment count")
     ap.add_argument("--no-overlap", dest="overlap", action="store_false",

@@ -358,7 +358,8 @@ def autotune(frames: int, height: int, width: int, bins: int, bin_range=None, de
     return {"segments": best[0], "tail_pct": best[1], "tail_div": best[2],
             "skew": bool(best[3] & 4),
             "bins_per_cta": 2 if best[3] & 8 else 4 if best[3] & 16 else None,
-            "ms": {key(k): round(v, 4) for k, v in times.items()}}
+            "ms": {key(k): round(v, 4) for k, v in times.items()},
+            "ranked": [list(k) + [round(v, 4)] for k, v in sorted(times.items(), key=lambda x: x[1])]}
 
 
 class GraphedIntegralHistogram:
