@@ -16,7 +16,7 @@ for name, fn in [("integral_histogram", lambda: device.integral_histogram(img, l
     print(name, round(dt * 1e6, 1), "us per call (host)", flush=True)
 L = _native.lib()
 import ctypes
-info = (ctypes.c_int64 * 15)()
+info = (ctypes.c_int64 * 16)()  # ih_plan_describe fills 16 entries (ABI 1.7)
 t0 = time.perf_counter()
 for _ in range(20000): L.ih_plan_describe(1, 1080, 1920, 32, 0, 1, info)
 print("ih_plan_describe raw", round((time.perf_counter() - t0) / 20000 * 1e6, 2), "us")
