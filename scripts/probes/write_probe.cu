@@ -117,9 +117,10 @@ __global__ void k2like_planeorder(uint32_t* out, int H, int W, int nb, int S) {
 // and thread 0 stores each tile with one tensor copy, NBUF-buffered.
 template <int NP, int R, int BOXW, int NBUF>
 __global__ void k2like_tmap(const __grid_constant__ CUtensorMap tm, int H, int W, int nb, int S) {
-  extern __shared__ __align__(1024) uint32_t st[];  // [NBUF][NP][nbox][R][BOXW]
+  extern __shared__ __align__(1024) uint32_t st[];  // [NBUF][NP][nbox][TS]
+  constexpr int TS = (R * BOXW + 31) / 32 * 32;    // tile stride: 128-byte aligned tiles
   const int g = blockIdx.x, s = blockIdx.y, f = blockIdx.z;
-  const int nbox = W / BOXW, per = NP * nbox * R * BOXW;
+  const int nbox = W / BOXW, per = NP * nbox * TS;
   const int r0 = s * S, r1 = min(r0 + S, H);
   for (int r = r0, k = 0; r < r1; r += R, ++k) {
     uint32_t* buf = st + (k % NBUF) * per;
@@ -135,7 +136,7 @@ __global__ void k2like_tmap(const __grid_constant__ CUtensorMap tm, int H, int W
           const int y = (int)(((int64_t)f * nb + g * NP + i) * H + r), x = bx * BOXW;
           asm volatile(
               "cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(&tm),
-              "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(buf + (i * nbox + bx) * R * BOXW))
+              "r"(x), "r"(y), "r"((uint32_t)__cvta_generic_to_shared(buf + (i * nbox + bx) * TS))
               : "memory");
         }
       asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -168,7 +169,7 @@ __global__ void k2like(uint32_t* out, int H, int W, int nb, int S) {
   }
 }
 
-int main() {
+int main(int argc, char** argv) {
   const int H = 1080, W = 1920, nb = 32, F = 64;
   const size_t elems = (size_t)F * nb * H * W;
   uint32_t* out;
@@ -189,6 +190,57 @@ int main() {
     printf("{\"probe\": \"%s\", \"ms\": %.4f, \"gbs\": %.1f}\n", name, ms, elems * 4 / ms / 1e6);
   };
   timeit("memset", [&] { cudaMemsetAsync(out, 0, elems * 4); });
+  // 2-D tensor-map TMA stores of staged [R x 240] tiles, against K2's 16-byte
+  // stores and 1-D bulk row copies above (same grid and segments)
+  {
+    CUtensorMap tm;
+    cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)F * nb * H};
+    cuuint64_t strides[1] = {(cuuint64_t)W * 4};
+    cuuint32_t box[2] = {240, 1}, estr[2] = {1, 1};
+    auto enc = [&](int rows) {
+      box[1] = rows;
+      CUresult cr = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides, box, estr,
+                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (cr != CUDA_SUCCESS) printf("{\"error\": \"cuTensorMapEncodeTiled %d\"}\n", (int)cr);
+    };
+    for (int nseg : {5, 9}) {
+      const int S = (H + nseg - 1) / nseg;
+      char nm[64];
+      enc(1);
+      {
+        const int sm = 2 * 4 * 8 * 256 * 4;
+        cudaFuncSetAttribute(k2like_tmap<4, 1, 240, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        snprintf(nm, sizeof nm, "k2like_tmap2d_np4_r1_nbuf2_nseg%d", nseg);
+        timeit(nm, [&] { k2like_tmap<4, 1, 240, 2><<<dim3(nb / 4, nseg, F), 480, sm>>>(tm, H, W, nb, S); });
+      }
+      enc(2);
+      {
+        const int sm = 2 * 2 * 2 * W * 4;
+        cudaFuncSetAttribute(k2like_tmap<2, 2, 240, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        snprintf(nm, sizeof nm, "k2like_tmap2d_np2_r2_nbuf2_nseg%d", nseg);
+        timeit(nm, [&] { k2like_tmap<2, 2, 240, 2><<<dim3(nb / 2, nseg, F), 480, sm>>>(tm, H, W, nb, S); });
+      }
+      enc(4);
+      {
+        const int sm = 4 * 4 * W * 4;
+        cudaFuncSetAttribute(k2like_tmap<4, 4, 240, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+        snprintf(nm, sizeof nm, "k2like_tmap2d_np4_r4_nbuf1_nseg%d", nseg);
+        timeit(nm, [&] { k2like_tmap<4, 4, 240, 1><<<dim3(nb / 4, nseg, F), 480, sm>>>(tm, H, W, nb, S); });
+      }
+      // K2's own pattern for comparison in the same run
+      snprintf(nm, sizeof nm, "k2like_cs_np4_nseg%d_ref", nseg);
+      timeit(nm, [&] { k2like<true, 4><<<dim3(nb / 4, nseg, F), 480>>>(out, H, W, nb, S); });
+      snprintf(nm, sizeof nm, "k2like_tma_np4_nseg%d_ref", nseg);
+      cudaFuncSetAttribute(k2like_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * W * 4);
+      timeit(nm, [&] { k2like_tma<4><<<dim3(nb / 4, nseg, F), 480, 2 * 4 * W * 4>>>(out, H, W, nb, S); });
+    }
+  }
+  if (argc > 1) {  // "tmap": only the tensor-map section
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
+    return 0;
+  }
   timeit("linear_cs", [&] { linear<true><<<148 * 8, 256>>>(out, elems / 4); });
   timeit("linear_wb", [&] { linear<false><<<148 * 8, 256>>>(out, elems / 4); });
   timeit("linear_v8", [&] { linear_v8<<<148 * 8, 256>>>(out, elems / 8); });
@@ -303,52 +355,6 @@ int main() {
     printf("{\"probe\": \"cfg1_memset_bufs8\", \"us_per_launch\": %.2f}\n", ms * 1000 / 20);
   }
 
-  // 2-D tensor-map TMA stores of staged [R x 240] tiles, against K2's 16-byte
-  // stores and 1-D bulk row copies above (same grid and segments)
-  {
-    CUtensorMap tm;
-    cuuint64_t dims[2] = {(cuuint64_t)W, (cuuint64_t)F * nb * H};
-    cuuint64_t strides[1] = {(cuuint64_t)W * 4};
-    cuuint32_t box[2] = {240, 1}, estr[2] = {1, 1};
-    auto enc = [&](int rows) {
-      box[1] = rows;
-      CUresult cr = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_UINT32, 2, out, dims, strides, box, estr,
-                                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                           CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (cr != CUDA_SUCCESS) printf("{\"error\": \"cuTensorMapEncodeTiled %d\"}\n", (int)cr);
-    };
-    for (int nseg : {5, 9}) {
-      const int S = (H + nseg - 1) / nseg;
-      char nm[64];
-      enc(1);
-      {
-        const int sm = 2 * 4 * W * 4;
-        cudaFuncSetAttribute(k2like_tmap<4, 1, 240, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        snprintf(nm, sizeof nm, "k2like_tmap2d_np4_r1_nbuf2_nseg%d", nseg);
-        timeit(nm, [&] { k2like_tmap<4, 1, 240, 2><<<dim3(nb / 4, nseg, F), 480, sm>>>(tm, H, W, nb, S); });
-      }
-      enc(2);
-      {
-        const int sm = 2 * 2 * 2 * W * 4;
-        cudaFuncSetAttribute(k2like_tmap<2, 2, 240, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        snprintf(nm, sizeof nm, "k2like_tmap2d_np2_r2_nbuf2_nseg%d", nseg);
-        timeit(nm, [&] { k2like_tmap<2, 2, 240, 2><<<dim3(nb / 2, nseg, F), 480, sm>>>(tm, H, W, nb, S); });
-      }
-      enc(4);
-      {
-        const int sm = 4 * 4 * W * 4;
-        cudaFuncSetAttribute(k2like_tmap<4, 4, 240, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-        snprintf(nm, sizeof nm, "k2like_tmap2d_np4_r4_nbuf1_nseg%d", nseg);
-        timeit(nm, [&] { k2like_tmap<4, 4, 240, 1><<<dim3(nb / 4, nseg, F), 480, sm>>>(tm, H, W, nb, S); });
-      }
-      // K2's own pattern for comparison in the same run
-      snprintf(nm, sizeof nm, "k2like_cs_np4_nseg%d_ref", nseg);
-      timeit(nm, [&] { k2like<true, 4><<<dim3(nb / 4, nseg, F), 480>>>(out, H, W, nb, S); });
-      snprintf(nm, sizeof nm, "k2like_tma_np4_nseg%d_ref", nseg);
-      cudaFuncSetAttribute(k2like_tma<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 4 * W * 4);
-      timeit(nm, [&] { k2like_tma<4><<<dim3(nb / 4, nseg, F), 480, 2 * 4 * W * 4>>>(out, H, W, nb, S); });
-    }
-  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) printf("error %s\n", cudaGetErrorString(e));
   return 0;
