@@ -74,7 +74,8 @@ size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width,
  *   lut256        HOST pointer, 256 entries, each < bins (BinSpec.table)
  *   bins          total bin count of the spec, 1..256 (core.py:72-73)
  *   bin_lo/hi     the slab this call produces (bin sharding; 0/bins = all)
- *   out           device, (frames, bin_hi-bin_lo, height, width) uint32
+ *   out           device, (frames, bin_hi-bin_lo, height, width) uint32,
+ *                 16-byte aligned when width % 4 == 0 (4-byte otherwise)
  *   workspace     device scratch of >= ih_workspace_bytes(...) bytes,
  *                 16-byte aligned.  Contents need no initialisation.
  *
@@ -83,7 +84,8 @@ size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width,
  *                    >= bins, bad slab, null pointers
  *   IH_ERR_CAPACITY  width*height > 2^32-1
  *   IH_ERR_PARAM     img_pitch < width, frame_stride < height*img_pitch,
- *                    workspace too small, unknown kernel
+ *                    workspace too small, unknown kernel, misaligned out or
+ *                    workspace (checked before any launch)
  *   IH_ERR_CUDA      launch failure */
 ih_status ih_integral_histogram(const uint8_t *img, int64_t frames, int64_t height,
                                 int64_t width, int64_t img_pitch, int64_t frame_stride,

@@ -1027,6 +1027,22 @@ size_t ih_workspace_bytes(int64_t frames, int64_t height, int64_t width, int32_t
   return n;
 }
 
+// Buffer alignment the kernels rely on: 16-byte output stores when every row
+// starts 16-byte aligned (width % 4 == 0), 4-byte elements otherwise; uint4
+// workspace slots.  Checked before any launch: a misaligned vector store
+// would fault and poison the caller's CUDA context.
+ih_status check_buffers(const Call& c, const void* out, bool need_out, const void* ws) {
+  if (need_out) {
+    if (!out) return fail(IH_ERR_PARAM, "null output pointer");
+    const uintptr_t a = c.W % 4 == 0 ? 15u : 3u;
+    if ((uintptr_t)out & a)
+      return fail(IH_ERR_PARAM, c.W % 4 == 0 ? "out must be 16-byte aligned when width % 4 == 0"
+                                             : "out must be 4-byte aligned");
+  }
+  if (ws && ((uintptr_t)ws & 15)) return fail(IH_ERR_PARAM, "workspace must be 16-byte aligned");
+  return IH_OK;
+}
+
 ih_status ih_ih_prepare(const uint8_t* img, int64_t frames, int64_t height, int64_t width,
                         int64_t img_pitch, int64_t frame_stride, const uint8_t* lut256,
                         int32_t bins, int32_t bin_lo, int32_t bin_hi, void* workspace,
@@ -1034,6 +1050,8 @@ ih_status ih_ih_prepare(const uint8_t* img, int64_t frames, int64_t height, int6
   Call c;
   ih_status st = validate(img, frames, height, width, img_pitch, frame_stride, lut256, bins,
                           bin_lo, bin_hi, kernel, &c);
+  if (st != IH_OK) return st;
+  st = check_buffers(c, nullptr, false, workspace);
   if (st != IH_OK) return st;
   c.stream = (cudaStream_t)stream;
   return launch_prepare(c, workspace, workspace_bytes);
@@ -1047,6 +1065,8 @@ ih_status ih_ih_scan(const uint8_t* img, int64_t frames, int64_t height, int64_t
   ih_status st = validate(img, frames, height, width, img_pitch, frame_stride, lut256, bins,
                           bin_lo, bin_hi, kernel, &c);
   if (st != IH_OK) return st;
+  st = check_buffers(c, out, true, workspace);
+  if (st != IH_OK) return st;
   c.stream = (cudaStream_t)stream;
   return launch_scan(c, out, workspace, workspace_bytes);
 }
@@ -1059,6 +1079,8 @@ ih_status ih_integral_histogram(const uint8_t* img, int64_t frames, int64_t heig
   Call c;
   ih_status st = validate(img, frames, height, width, img_pitch, frame_stride, lut256, bins,
                           bin_lo, bin_hi, kernel, &c);
+  if (st != IH_OK) return st;
+  st = check_buffers(c, out, true, workspace);
   if (st != IH_OK) return st;
   c.stream = (cudaStream_t)stream;
   st = launch_prepare(c, workspace, workspace_bytes);

@@ -433,10 +433,7 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
     if out is None:
         out = empty_output(a.frames, nb, a.H, a.W, a.dev)
     else:
-        if out.dtype not in (torch.uint32, torch.int32) or not out.is_contiguous():
-            raise ShapeError("out must be a contiguous uint32 tensor")
-        if out.numel() != a.frames * nb * a.H * a.W or out.device != a.dev:
-            raise ShapeError("out has the wrong size or device")
+        _check_ih_out(out, a, nb)
     ws = _workspace_for(a, workspace)
     L = _native.lib()
     with _on_device(a.dev):  # launches go to the tensors' device
@@ -447,6 +444,17 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
     if squeeze and out.dim() == 4:
         return out[0]
     return out
+
+
+def _check_ih_out(out, a: "_Args", nb: int) -> None:
+    """A caller-provided output of integral_histogram / scan: contiguous
+    uint32 (or int32) with frames*nb*H*W elements on the images' device.  The
+    C ABI also rejects a misaligned pointer (16 bytes when W % 4 == 0)."""
+    if not isinstance(out, torch.Tensor) or out.dtype not in (torch.uint32, torch.int32) or \
+            not out.is_contiguous():
+        raise ShapeError("out must be a contiguous uint32 tensor")
+    if out.numel() != a.frames * nb * a.H * a.W or out.device != a.dev:
+        raise ShapeError("out has the wrong size or device")
 
 
 def _workspace_for(a: "_Args", workspace) -> torch.Tensor:
@@ -478,6 +486,10 @@ def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None,
          workspace=None) -> torch.Tensor:
     """Phase 2 of integral_histogram (the dominant single-pass kernel)."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
+    nb = a.hi - a.lo
+    if nb < 1 or a.lo < 0 or a.hi > a.bins:
+        raise ShapeError("bin slab must satisfy 0 <= lo < hi <= bins")
+    _check_ih_out(out, a, nb)
     ws = _workspace_for(a, workspace)
     with _on_device(a.dev):
         _native.check(_native.lib().ih_ih_scan(

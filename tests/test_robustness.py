@@ -95,6 +95,42 @@ def test_window_counts_misaligned_out():
 
 
 @gpu
+def test_integral_histogram_misaligned_out_is_rejected():
+    """A uint32 out view 4 bytes past a 16-byte boundary with W % 4 == 0 (the
+    kernels' 16-byte stores would fault) is refused before any launch; the
+    same view is fine for an odd width (alignment-adaptive stores), and the
+    context stays usable."""
+    import torch
+
+    from paper_1711_01919_b200 import device
+    from paper_1711_01919_b200.errors import ParameterError, ShapeError
+
+    table = O.np_uniform_table(8)
+    for W, ok in ((64, False), (61, True)):
+        px = np.random.default_rng(W).integers(0, 256, (33, W), dtype=np.uint8)
+        img = device.upload_image(px)
+        n = 8 * 33 * W
+        buf = torch.zeros(n + 1, dtype=torch.uint32, device="cuda")
+        out = buf[1:].view(8, 33, W)
+        assert out.data_ptr() % 16 == 4
+        if ok:
+            device.integral_histogram(img, table, 8, out=out)
+            assert np.array_equal(out.cpu().numpy(), O.compute_sequential(px, table, 8))
+        else:
+            with pytest.raises(ParameterError, match="16-byte aligned"):
+                device.integral_histogram(img, table, 8, out=out)
+            with pytest.raises(ParameterError, match="16-byte aligned"):
+                device.scan(img, table, 8, out)
+        with pytest.raises(ShapeError):
+            device.scan(img, table, 8, buf[: n // 2])  # too small: refused, not written past
+    # the context is intact
+    px = np.random.default_rng(0).integers(0, 256, (16, 16), dtype=np.uint8)
+    t = device.integral_histogram(device.upload_image(px), table, 8)
+    torch.cuda.synchronize()
+    assert np.array_equal(t.cpu().numpy(), O.compute_sequential(px, table, 8))
+
+
+@gpu
 def test_explicit_stream_queries():
     import torch
 
