@@ -22,7 +22,7 @@ import torch
 from . import _native
 from .errors import BoundsError, DeviceError, ParameterError, ShapeError
 
-_workspaces: dict[int, torch.Tensor] = {}
+_workspaces: dict[tuple, torch.Tensor] = {}
 _cuda_seen = False  # a CUDA device was visible once (availability cannot go away)
 _NULLCTX = contextlib.nullcontext()
 
@@ -60,17 +60,21 @@ def _on_device(dev: torch.device):
     return _NULLCTX if torch.cuda.current_device() == dev.index else torch.cuda.device(dev)
 
 
-def workspace_(dev: torch.device, nbytes: int) -> torch.Tensor:
-    """Per-device scratch buffer, grown on demand (caller-owned per the ABI)."""
-    idx = dev.index
-    ws = _workspaces.get(idx)
+def workspace_(dev: torch.device, nbytes: int, stream: int = 0) -> torch.Tensor:
+    """Scratch buffer per (device, stream), grown on demand (caller-owned per
+    the ABI).  Calls on one stream are ordered, so they can share it; calls on
+    different streams (threads, pipelines) get different buffers."""
+    key = (dev.index, int(stream))
+    ws = _workspaces.get(key)
     if ws is None or ws.numel() < nbytes:
         ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
-        _workspaces[idx] = ws
+        _workspaces[key] = ws
     return ws
 
 
-_lut_last: list = [None, 0]  # [last uint8 table array (kept alive), its data pointer]
+# (last uint8 table array (kept alive), its data pointer): one tuple, replaced
+# as a whole, so a thread never pairs one table with another's pointer
+_lut_last: tuple = (None, 0)
 
 
 def _lut_array(table) -> np.ndarray:
@@ -84,11 +88,13 @@ def _lut_ptr(a: "_Args") -> int:
     """Host address of the call's 256-byte table (read by the C ABI during the
     call).  A table that already is a contiguous uint8 array is used in place,
     so its pointer is cached per table object."""
+    global _lut_last
     lut = a.lut
-    if _lut_last[0] is lut:
-        return _lut_last[1]
+    last = _lut_last
+    if last[0] is lut:
+        return last[1]
     ptr = lut.ctypes.data
-    _lut_last[0], _lut_last[1] = lut, ptr
+    _lut_last = (lut, ptr)
     return ptr
 
 
@@ -422,8 +428,9 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
     the bin-major tensor of IntegralHistogram.counts (core.py:106-116) for the
     bins [lo, hi) of ``bin_range`` (default: all).  Bit-identical to every
     reference strategy (strategies.py:109-229).  The default scratch buffer is
-    per device: concurrent calls on different streams pass their own
-    ``workspace`` (a uint8 CUDA tensor of ``workspace_bytes(...)`` bytes).
+    per (device, stream), so concurrent calls on different streams do not
+    share it; ``workspace`` (a uint8 CUDA tensor of ``workspace_bytes(...)``
+    bytes) overrides it.
     """
     squeeze = images.dim() == 2 and out is None
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
@@ -457,10 +464,14 @@ def _check_ih_out(out, a: "_Args", nb: int) -> None:
         raise ShapeError("out has the wrong size or device")
 
 
-def _workspace_for(a: "_Args", workspace) -> torch.Tensor:
+def _workspace_for(a: "_Args", workspace, per_stream: bool = True) -> torch.Tensor:
+    """The call's scratch: ``workspace`` if given, else the default buffer of
+    (device, stream) -- or of the device alone for the prepare/scan split,
+    whose two halves may be issued on different (caller-synchronised)
+    streams and must find the same carries."""
     need = _native.lib().ih_workspace_bytes(a.frames, a.H, a.W, a.hi - a.lo, a.kernel)
     if workspace is None:
-        return workspace_(a.dev, need)
+        return workspace_(a.dev, need, a.stream if per_stream else 0)
     if workspace.numel() * workspace.element_size() < need or not workspace.is_cuda:
         raise ParameterError(f"workspace needs {need} bytes on the device")
     return workspace
@@ -474,7 +485,7 @@ def prepare(images, table, bins, bin_range=None, kernel="auto", stream=None,
     batch, the phase for batch k+1 can run on a side stream while batch k's
     scan (write-bound) runs."""
     a = _prepare_args(images, table, bins, bin_range, kernel, stream)
-    ws = _workspace_for(a, workspace)
+    ws = _workspace_for(a, workspace, per_stream=False)
     with _on_device(a.dev):
         _native.check(_native.lib().ih_ih_prepare(
             a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, _lut_ptr(a),
@@ -490,7 +501,7 @@ def scan(images, table, bins, out, bin_range=None, kernel="auto", stream=None,
     if nb < 1 or a.lo < 0 or a.hi > a.bins:
         raise ShapeError("bin slab must satisfy 0 <= lo < hi <= bins")
     _check_ih_out(out, a, nb)
-    ws = _workspace_for(a, workspace)
+    ws = _workspace_for(a, workspace, per_stream=False)
     with _on_device(a.dev):
         _native.check(_native.lib().ih_ih_scan(
             a.images.data_ptr(), a.frames, a.H, a.W, a.pitch, a.fstride, _lut_ptr(a),

@@ -131,6 +131,45 @@ def test_integral_histogram_misaligned_out_is_rejected():
 
 
 @gpu
+def test_concurrent_calls_on_threads_and_streams():
+    """Two host threads, each on its own CUDA stream with its own bin table,
+    calling integral_histogram with the default workspace: every result is the
+    oracle's (per-(device, stream) scratch, atomic table-pointer cache)."""
+    import threading
+
+    import torch
+
+    from paper_1711_01919_b200 import device
+
+    px = np.random.default_rng(11).integers(0, 256, (96, 200), dtype=np.uint8)
+    img = device.upload_image(px)
+    want = {b: O.compute_sequential(px, O.np_uniform_table(b), b) for b in (7, 32)}
+    errors = []
+
+    def worker(bins):
+        try:
+            s = torch.cuda.Stream()
+            table = O.np_uniform_table(bins)
+            with torch.cuda.stream(s):
+                for _ in range(40):
+                    t = device.integral_histogram(img, table, bins)
+                    s.synchronize()
+                    if not np.array_equal(t.cpu().numpy(), want[bins]):
+                        errors.append(bins)
+                        return
+        except Exception as e:  # surfaced below
+            errors.append(repr(e))
+
+    torch.cuda.synchronize()
+    th = [threading.Thread(target=worker, args=(b,)) for b in (7, 32)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errors, errors
+
+
+@gpu
 def test_explicit_stream_queries():
     import torch
 
