@@ -818,6 +818,9 @@ ih_status launch_prepare(const Call& c, void* ws, size_t ws_bytes) {
       cw >>= 1;
     const int64_t force = env_int("IH_COUNT_CW", 0);
     if (force == 1 || force == 2 || force == 4 || force == 8) cw = (int)force;
+    // a forced width still has to fit the per-CTA shared tables (256 bins:
+    // 66 KB per chunk; the opt-in maximum is 227 KB)
+    while (cw > 1 && (size_t)cw * table_bytes > (200u << 10)) cw >>= 1;
     return cw;
   };
   if (p.nbp <= ih::kGroup && !p.colt && env_int("IH_COLCOUNTS_G1", 1) != 0 &&
