@@ -1127,7 +1127,9 @@ ih_status ih_window_counts(const uint32_t* t, int32_t nb, int64_t height, int64_
   // and a 16-byte aligned `out`; otherwise mode 3
   int64_t k4mode = env_int("IH_K4_MODE", 4);
   if (k4mode == 4 && (width % 4 != 0 || ((uintptr_t)t & 15) || ((uintptr_t)out & 15))) k4mode = 3;
-  if (k4mode == 3 && ((uintptr_t)out & 15)) k4mode = 1;
+  // modes 2 and 3 store 16-byte pairs: an `out` 8 bytes past a 16-byte
+  // boundary takes the 8-byte-store kernel
+  if ((k4mode == 2 || k4mode == 3) && ((uintptr_t)out & 15)) k4mode = 1;
   if ((uintptr_t)out & 7) return fail(IH_ERR_PARAM, "out must be 8-byte aligned");
   if (k4mode == 4) {
     const int64_t cb = (C + 4 * 256 - 1) / (4 * 256);

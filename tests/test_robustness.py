@@ -76,22 +76,26 @@ def test_kernel_never_reads_outside_for_invalid_regions():
 
 
 @gpu
-def test_window_counts_misaligned_out():
-    """An int64 out view at an odd element offset (8- but not 16-byte aligned)."""
+@pytest.mark.parametrize("mode", ["0", "1", "2", "3", "4"])
+def test_window_counts_misaligned_out(monkeypatch, mode):
+    """An int64 out view at an odd element offset (8- but not 16-byte aligned),
+    for every K4 kernel (IH_K4_MODE; the 16-byte-pair modes fall back)."""
     import torch
 
     from paper_1711_01919_b200 import device
 
+    monkeypatch.setenv("IH_K4_MODE", mode)
     px = np.random.default_rng(3).integers(0, 256, (30, 41), dtype=np.uint8)
     t = device.integral_histogram(device.upload_image(px), O.np_uniform_table(5), 5)
-    shape = (5, 30 - 4 + 1, 41 - 6 + 1)
-    n = int(np.prod(shape))
-    buf = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
-    out = buf[1:].view(shape)
-    assert out.data_ptr() % 16 == 8
-    device.window_counts(t, 4, 6, out=out)
-    want = O.window_counts(O.compute_sequential(px, O.np_uniform_table(5), 5), 4, 6)
-    assert np.array_equal(out.cpu().numpy(), want)
+    for h, w in ((4, 6), (1, 40), (7, 7)):  # odd and even output row lengths
+        shape = (5, 30 - h + 1, 41 - w + 1)
+        n = int(np.prod(shape))
+        buf = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+        out = buf[1:].view(shape)
+        assert out.data_ptr() % 16 == 8
+        device.window_counts(t, h, w, out=out)
+        want = O.window_counts(O.compute_sequential(px, O.np_uniform_table(5), 5), h, w)
+        assert np.array_equal(out.cpu().numpy(), want), (h, w)
 
 
 @gpu
