@@ -67,9 +67,21 @@ def workspace_(dev: torch.device, nbytes: int, stream: int = 0) -> torch.Tensor:
     key = (dev.index, int(stream))
     ws = _workspaces.get(key)
     if ws is None or ws.numel() < nbytes:
+        if ws is not None:
+            # kernels queued on `stream` may still read the old buffer, and the
+            # caching allocator only orders its reuse against the stream it was
+            # allocated on: wait for them (growth is rare), or, inside a graph
+            # capture where a sync is illegal, keep the old buffer alive
+            if torch.cuda.is_current_stream_capturing():
+                _retired.append(ws)
+            else:
+                torch.cuda.synchronize(dev)
         ws = torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
         _workspaces[key] = ws
     return ws
+
+
+_retired: list = []  # workspaces outgrown during a graph capture (never freed)
 
 
 # (last uint8 table array (kept alive), its data pointer): one tuple, replaced

@@ -174,6 +174,32 @@ def test_concurrent_calls_on_threads_and_streams():
 
 
 @gpu
+def test_default_workspace_grows_under_queued_work():
+    """Calls on an explicit side stream whose default workspace must grow
+    while earlier calls are still queued: the old buffer is not recycled
+    under them (each result equals the oracle)."""
+    import torch
+
+    from paper_1711_01919_b200 import device
+
+    s = torch.cuda.Stream()
+    table = O.np_uniform_table(16)
+    rng = np.random.default_rng(21)
+    shapes = [(40, 300), (300, 1000), (900, 1900), (1080, 1920)]  # growing workspaces
+    pxs = [rng.integers(0, 256, sh, dtype=np.uint8) for sh in shapes]
+    imgs = [device.upload_image(p) for p in pxs]
+    torch.cuda.synchronize()
+    outs = []
+    for _ in range(3):
+        for img in imgs:
+            outs.append(device.integral_histogram(img, table, 16, stream=s))
+    s.synchronize()
+    for k, t in enumerate(outs):
+        px = pxs[k % len(pxs)]
+        assert np.array_equal(t.cpu().numpy(), O.compute_sequential(px, table, 16)), k
+
+
+@gpu
 def test_explicit_stream_queries():
     import torch
 
