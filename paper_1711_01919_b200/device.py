@@ -449,8 +449,9 @@ def integral_histogram(images: torch.Tensor, table, bins: int, bin_range=None, o
     nb = a.hi - a.lo
     if nb < 1 or a.lo < 0 or a.hi > a.bins:
         raise ShapeError("bin slab must satisfy 0 <= lo < hi <= bins")
-    if out is None:
-        out = empty_output(a.frames, nb, a.H, a.W, a.dev)
+    if out is None:  # allocated on the launch stream, so its reuse is ordered after the kernels
+        with (torch.cuda.stream(stream) if stream is not None else _NULLCTX):
+            out = empty_output(a.frames, nb, a.H, a.W, a.dev)
     else:
         _check_ih_out(out, a, nb)
     ws = _workspace_for(a, workspace)
@@ -659,8 +660,9 @@ def likelihood_map(t: torch.Tensor, template, h: int, w: int, metric: str = "bha
     if h > H or w > W:
         raise BoundsError(f"{h}x{w} window exceeds {W}x{H} image")
     shape = (H - h + 1, W - w + 1)
-    out = torch.empty(shape, dtype=torch.float64, device=t.device) if out is None else \
-        _check_out(out, shape, (torch.float64,), t.device)
+    with torch.cuda.device(t.device), (torch.cuda.stream(stream) if stream is not None else _NULLCTX):
+        out = torch.empty(shape, dtype=torch.float64, device=t.device) if out is None else \
+            _check_out(out, shape, (torch.float64,), t.device)
     L = _native.lib()
     nws = int(L.ih_likelihood_workspace_bytes(nb, int(h), int(w)))
     with torch.cuda.device(t.device):
